@@ -1,0 +1,72 @@
+#!/usr/bin/env python3
+"""Generate the golden fixtures that pin the CPU oracle.
+
+Runs the UNMODIFIED reference library (compiled in place from
+/root/reference/proj/src by `make -C oracle ref`, linked with the builder's
+stand-in coarse solver and harness -> oracle/_ref/ref_harness) and stores its
+outputs as small JSON fixtures in tests/golden/. Run in the build container
+(it needs /root/reference); the fixtures are committed and travel to the GPU
+box, where /root/reference does not exist.
+
+    python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[2]
+HARNESS = ROOT / "oracle" / "_ref" / "ref_harness"
+OUT = Path(__file__).resolve().parent
+
+# (file stem, harness argv)
+STRUCTURE = [
+    ("struct_square_2_full", ["structure", "square", "2", "neumann", "full"]),
+    ("struct_square_2_dirichlet_full", ["structure", "square", "2", "dirichlet", "full"]),
+    ("struct_ico_1_full", ["structure", "ico", "1", "neumann", "full"]),
+    ("struct_equi_4_8_1", ["structure", "equi:4:8:1.0", "1", "neumann", "full"]),
+    ("struct_grid_3_2", ["structure", "grid:3:2:2.0:1.5", "2", "neumann"]),
+    ("struct_square_4", ["structure", "square", "4", "neumann"]),
+    ("struct_square_4_dirichlet", ["structure", "square", "4", "dirichlet"]),
+    ("struct_ico_4", ["structure", "ico", "4", "neumann"]),
+    ("struct_ico_6", ["structure", "ico", "6", "neumann"]),
+    ("struct_equi_4_8_3", ["structure", "equi:4:8:1.0", "3", "neumann"]),
+]
+CYCLES = [
+    ("cycles_square_4_dirichlet_sinsin", ["cycles", "square", "4", "dirichlet", "sinsin", "0", "12"]),
+    ("cycles_square_4_uniform", ["cycles", "square", "4", "neumann", "uniform", "1", "12"]),
+    ("cycles_ico_4_uniform", ["cycles", "ico", "4", "neumann", "uniform", "1", "10"]),
+    ("cycles_ico_5_ylm", ["cycles", "ico", "5", "neumann", "ylm", "2", "8"]),
+    ("cycles_equi_4_8_3_lr", ["cycles", "equi:4:8:1.0", "3", "neumann", "lr", "3", "10"]),
+    ("cycles_ico_3_uniform_gs", ["cycles", "ico", "3", "neumann", "uniform", "4", "6", "gs"]),
+]
+SOLVES = [
+    # BASELINE configs 1-3 (config 3 takes ~30 s of reference setup)
+    ("solve_config1", ["solve", "square", "4", "dirichlet", "sinsin", "0", "1e-8", "200"]),
+    ("solve_config2", ["solve", "ico", "6", "neumann", "ylm", "1", "1e-8", "200"]),
+    ("solve_config3", ["solve", "ico", "8", "neumann", "uniform", "1", "1e-8", "200"]),
+    ("solve_equi_4_8_3_lr", ["solve", "equi:4:8:1.0", "3", "neumann", "lr", "23", "1e-10", "50"]),
+    ("solve_square_6_uniform", ["solve", "square", "6", "neumann", "uniform", "5", "1e-8", "200"]),
+]
+
+
+def run(argv):
+    res = subprocess.run([str(HARNESS), *argv], check=True, capture_output=True, text=True)
+    return json.loads(res.stdout)
+
+
+def main() -> int:
+    if not HARNESS.exists():
+        subprocess.run(["make", "-C", str(ROOT / "oracle"), "ref", "-j8"], check=True)
+    for stem, argv in STRUCTURE + CYCLES + SOLVES:
+        data = run(argv)
+        data["_argv"] = argv
+        (OUT / f"{stem}.json").write_text(json.dumps(data, separators=(",", ":")) + "\n")
+        print(stem, file=sys.stderr)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
