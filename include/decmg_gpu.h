@@ -1,0 +1,168 @@
+/*
+ * decmg_gpu -- B200-native (sm_100a) geometric multigrid for the DEC 0-form
+ * Poisson problem on nested binary-subdivided triangle meshes.
+ *
+ * C ABI (plain pointers and sizes, no exceptions, no torch types). This is the
+ * drop-in boundary for the reference C++ library `decmg`
+ * (/root/reference/proj); every entry point names the reference interface it
+ * replaces. A header-only C++ shim with the reference's own class/function
+ * names and exception types is in include/decmg_gpu.hpp; INTEGRATION.md shows
+ * how a reference user binds it.
+ *
+ * Conventions
+ *  - Status codes: DECMG_OK (0) or one of the error classes below; the message
+ *    is available from decmg_gpu_last_error(ctx) (or decmg_gpu_last_error(NULL)
+ *    when creation failed).
+ *  - Vectors are row-major [n][nrhs] fp64 (the nrhs right-hand sides of one
+ *    vertex are adjacent). nrhs = 1 is the reference's single-vector case.
+ *  - Host-pointer entry points copy in/out synchronously and retain no pointer.
+ *    `_dev` entry points take device pointers and only enqueue work on the
+ *    context's stream (decmg_gpu_stream).
+ *  - Level 0 is the finest level (reference order, proj/src/multigrid.cpp:196).
+ *  - One in-flight call per context; several contexts may run concurrently.
+ */
+#ifndef DECMG_GPU_H
+#define DECMG_GPU_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DECMG_API __attribute__((visibility("default")))
+#else
+#define DECMG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct decmg_gpu_ctx decmg_gpu_ctx;
+
+enum {
+    DECMG_OK = 0,
+    DECMG_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    DECMG_RUNTIME = 2,          /* std::runtime_error in the reference     */
+    DECMG_CUDA = 3,
+    DECMG_NCCL = 4,
+    DECMG_OOM = 5
+};
+
+/* creation flags */
+#define DECMG_PROJECT_SPHERE 1u /* push new midpoints to the unit sphere (x2)   */
+#define DECMG_DIRICHLET 2u      /* identity rows on boundary vertices (x1)      */
+
+typedef struct {
+    int device;   /* CUDA device ordinal                                    */
+    int max_nrhs; /* largest batch run_cycles/solve will see (1..32)        */
+} decmg_gpu_config;
+
+/* Hierarchy construction on the device: replaces
+ *   subdivision_tower (proj/src/subdivision.cpp:127-139) +
+ *   build_hierarchy / MultigridHierarchy ctor (proj/src/multigrid.cpp:196-238,325-341)
+ * including from_triangles (mesh.cpp:122-157), build_dual (dual.cpp:7-63),
+ * laplacian_0 (operators.cpp:102-122), matrix_of/transposed (multigrid.cpp:215)
+ * and restriction_matrix (geometric_map.cpp:205-223).
+ * `positions` [nv][3], `corner_triples` [nt][3] describe the base complex
+ * (as passed to EmbeddedComplex2D::from_triangles); nsub binary subdivisions. */
+DECMG_API int decmg_gpu_create_from_base(const double* positions, int nv, const int* corner_triples, int nt,
+                               int nsub, unsigned flags, const decmg_gpu_config* cfg,
+                               decmg_gpu_ctx** out);
+
+/* Upload an already assembled hierarchy (reference layout: CSR of L per level,
+ * P = prolongation n_k x n_{k+1}, R = restriction n_{k+1} x n_k, dual areas).
+ * Replaces MultigridHierarchy(meshes, maps) for callers that assemble on the
+ * host. boundary may be NULL (Neumann). */
+typedef struct {
+    int nv;
+    const int* L_row_ptr;
+    const int* L_col_idx;
+    const double* L_values;
+    int64_t L_nnz;
+    const double* dual_areas;
+    const int* boundary;
+    const int* P_row_ptr; /* NULL on the coarsest level */
+    const int* P_col_idx;
+    const double* P_values;
+    int64_t P_nnz;
+    const int* R_row_ptr;
+    const int* R_col_idx;
+    const double* R_values;
+    int64_t R_nnz;
+} decmg_gpu_level_desc;
+DECMG_API int decmg_gpu_create_from_levels(const decmg_gpu_level_desc* levels, int nlevels, unsigned flags,
+                                 const decmg_gpu_config* cfg, decmg_gpu_ctx** out);
+
+DECMG_API void decmg_gpu_destroy(decmg_gpu_ctx* ctx);
+DECMG_API const char* decmg_gpu_last_error(const decmg_gpu_ctx* ctx);
+
+/* CyclePlan (proj/include/decmg/multigrid.hpp:70-89). walk: 'd'/'u' string
+ * (NULL = the V walk of standard_plan, multigrid.cpp:171-194); pre/post:
+ * per-level sweep counts (NULL = pre_all/post_all on every level). */
+enum { DECMG_SMOOTHER_JACOBI = 0 };
+typedef struct {
+    const char* walk;
+    const int* pre;
+    const int* post;
+    int pre_all;
+    int post_all;
+    int smoother;
+    double jacobi_omega;
+} decmg_gpu_plan;
+
+/* MultigridHierarchy::run_cycle (proj/src/multigrid.cpp:287-323): ncycles
+ * cycles from x0 (NULL = zeros); x_out [n0][nrhs]; hist_out [ncycles][nrhs]
+ * = fine relative residual after each cycle. */
+DECMG_API int decmg_gpu_run_cycles(decmg_gpu_ctx* ctx, const decmg_gpu_plan* plan, int nrhs, const double* b,
+                         const double* x0, int ncycles, double* x_out, double* hist_out);
+
+/* gmg_solve (proj/src/solvers.cpp:251-279): projects b (Neumann), repeats
+ * one-cycle runs until every RHS has relative residual <= tol or max_cycles.
+ * hist_out [max_cycles][nrhs] (rows past *cycles_done untouched);
+ * final_out [nrhs] = recomputed final relative residual. */
+DECMG_API int decmg_gpu_solve(decmg_gpu_ctx* ctx, const decmg_gpu_plan* plan, int nrhs, const double* b,
+                    const double* x0, double tol, int max_cycles, double* x_out, double* hist_out,
+                    int* cycles_done, double* final_out);
+
+/* Device-pointer variants (inputs already resident in HBM). hist/final are
+ * device arrays too. */
+DECMG_API int decmg_gpu_run_cycles_dev(decmg_gpu_ctx* ctx, const decmg_gpu_plan* plan, int nrhs,
+                             const double* d_b, const double* d_x0, int ncycles, double* d_x,
+                             double* d_hist);
+DECMG_API void* decmg_gpu_stream(decmg_gpu_ctx* ctx); /* cudaStream_t of the context */
+
+/* MultigridHierarchy::project_compatible (proj/src/multigrid.cpp:240-250), in place. */
+DECMG_API int decmg_gpu_project_compatible(decmg_gpu_ctx* ctx, int nrhs, double* b);
+
+/* SparseOperator::apply (proj/src/sparse.cpp:209-218) of level k's operator
+ * op = 'L' (n_k x n_k), 'P' (n_k x n_{k+1}), 'R' (n_{k+1} x n_k). */
+DECMG_API int decmg_gpu_apply(decmg_gpu_ctx* ctx, int level, char op, const double* x, double* y);
+
+/* Structure export for parity. counts = {nv, ne, nt, nnz(L), nnz(P), nnz(R)}.
+ * name: positions, edges, triangles, corners, dual_areas, boundary, diag,
+ * L_row_ptr, L_col_idx, L_values, P_*, R_*. Returns the element count (query
+ * with out = NULL) or -1. hash = EmbeddedComplex2D::hash (mesh.cpp:112-119). */
+DECMG_API int decmg_gpu_levels(const decmg_gpu_ctx* ctx);
+DECMG_API int decmg_gpu_level_info(decmg_gpu_ctx* ctx, int level, int64_t counts[6]);
+DECMG_API int64_t decmg_gpu_export(decmg_gpu_ctx* ctx, int level, const char* name, void* out);
+DECMG_API int decmg_gpu_mesh_hash(decmg_gpu_ctx* ctx, int level, uint64_t* hash);
+
+/* Per-kernel device timing (CUDA events around every launch when enabled).
+ * Kernel classes: 0 fine sweep, 1 fine residual, 2 restrict, 3 prolong,
+ * 4 coarse-level work, 5 coarse solve, 6 norms. */
+DECMG_API int decmg_gpu_set_timing(decmg_gpu_ctx* ctx, int enable);
+DECMG_API int decmg_gpu_get_timing(decmg_gpu_ctx* ctx, int cls, int64_t* launches, double* total_ms,
+                         double* bytes);
+DECMG_API int64_t decmg_gpu_launch_count(decmg_gpu_ctx* ctx); /* kernels launched since creation */
+
+/* Input generators (extension x3): base meshes and synthetic RHS.
+ * base_mesh spec: "square", "ico", "grid:nx:ny:lx:ly", "equi:rows:cols:side".
+ * Query sizes with positions = corners = NULL. */
+DECMG_API int decmg_base_mesh(const char* spec, double* positions, int* nv, int* corners, int* nt);
+/* kind: "uniform" (2u-1), "ylm" (Y_3^2 + 1e-3 N(0,1)), "sinsin", "lr" (L*u);
+ * RHS j uses seed + j. Writes [n0][nrhs]. Dirichlet contexts zero boundary rows. */
+DECMG_API int decmg_gpu_make_rhs(decmg_gpu_ctx* ctx, const char* kind, uint64_t seed, int nrhs, double* b);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

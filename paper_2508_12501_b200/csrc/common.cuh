@@ -1,0 +1,177 @@
+// decmg_gpu internals shared by setup.cu, cycle.cu and capi.cu.
+//
+// All translation units are compiled with --fmad=false (see Makefile): the
+// reference is compiled with -ffp-contract=off, and every floating-point
+// expression below is written in the reference's evaluation order, so the
+// device produces the reference's bits.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/decmg_gpu.h"
+
+namespace decmg_gpu {
+
+// Error propagation without exceptions across the ABI.
+struct Status {
+    int code = DECMG_OK;
+    std::string msg;
+    bool ok() const { return code == DECMG_OK; }
+    static Status Ok() { return {}; }
+    static Status Err(int c, std::string m) { return {c, std::move(m)}; }
+};
+
+inline Status cuda_status(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return Status::Ok();
+    const int code = e == cudaErrorMemoryAllocation ? DECMG_OOM : DECMG_CUDA;
+    return Status::Err(code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define DG_TRY(expr)                         \
+    do {                                     \
+        ::decmg_gpu::Status _s = (expr);     \
+        if (!_s.ok()) return _s;             \
+    } while (0)
+#define DG_CUDA(call) DG_TRY(::decmg_gpu::cuda_status((call), #call))
+
+// One level of the hierarchy, device resident. Finest level is index 0.
+struct Level {
+    int nv = 0, ne = 0, nt = 0;
+    // complex (EmbeddedComplex2D, proj/include/decmg/mesh.hpp:32-86)
+    double* pos = nullptr;   // [nv][3]
+    int* edges = nullptr;    // [ne][2] src < tgt, lexicographic
+    int* tris = nullptr;     // [nt][3] (e0,e1,e2), e_i opposite corner i
+    int* corners = nullptr;  // [nt][3] (v0,v1,v2)
+    int* eptr = nullptr;     // [nv+1] edges with src == v
+    int* ve_ptr = nullptr;   // [nv+1] vertex -> incident edges (ascending)
+    int* ve = nullptr;       // [2 ne]
+    // operators
+    double* area = nullptr;  // dual cell areas (star0 diagonal)
+    int* bd = nullptr;       // boundary flag (extension x1)
+    double* diag = nullptr;  // L_ii
+    int* L_rp = nullptr;
+    int* L_ci = nullptr;
+    double* L_v = nullptr;
+    int64_t nnzL = 0;
+    // transfers to the next coarser level (absent on the coarsest)
+    int* P_rp = nullptr;
+    int* P_ci = nullptr;
+    double* P_v = nullptr;
+    int64_t nnzP = 0;
+    int* R_rp = nullptr;
+    int* R_ci = nullptr;
+    double* R_v = nullptr;
+    int64_t nnzR = 0;
+    int zero_diag_row = -1;  // first row with L_ii == 0 (-1: none)
+    double wtot = 0.0;       // sum of dual areas, sequential (coarse solve)
+    // work vectors [nv][max_nrhs]
+    double* x[2] = {nullptr, nullptr};
+    int cur = 0;
+    double* b = nullptr;
+    bool x_zero = false;     // x[cur] known to be exactly +0.0 (fresh descent)
+};
+
+struct Timing {
+    bool enabled = false;
+    struct Rec {
+        int cls;
+        double bytes;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    int64_t launches[8] = {};
+    double ms[8] = {};
+    double bytes[8] = {};
+};
+
+}  // namespace decmg_gpu
+
+struct decmg_gpu_ctx {
+    int device = 0;
+    int max_nrhs = 1;
+    unsigned flags = 0;
+    bool dirichlet = false;
+    cudaStream_t stream = nullptr;
+    std::vector<decmg_gpu::Level> lv;
+    double* r = nullptr;        // residual scratch [n0][max_nrhs]
+    double* red = nullptr;      // reduction partials
+    size_t red_cap = 0;         // doubles
+    double* dsmall = nullptr;   // per-RHS device scalars (256 doubles)
+    double* hsmall = nullptr;   // pinned host mirror
+    double* coarse_scratch = nullptr;
+    double* bproj = nullptr;    // projected RHS for solve [n0][max_nrhs]
+    double* xsol = nullptr;     // solve snapshot [n0][max_nrhs]
+    double* hist_dev = nullptr; // [hist_cap][max_nrhs]
+    int hist_cap = 0;
+    double* io_b = nullptr;     // staging for host-pointer calls [n0][max_nrhs]
+    double* io_x0 = nullptr;
+    double* io_x = nullptr;
+    int64_t launch_count = 0;
+    decmg_gpu::Timing timing;
+    std::string err;
+    std::vector<void*> allocations;
+};
+
+namespace decmg_gpu {
+
+// Device allocation owned by the context (freed in destroy).
+template <class T>
+Status dalloc(decmg_gpu_ctx* c, T** p, size_t n) {
+    void* q = nullptr;
+    DG_CUDA(cudaMalloc(&q, (n ? n : 1) * sizeof(T)));
+    c->allocations.push_back(q);
+    *p = static_cast<T*>(q);
+    return Status::Ok();
+}
+
+// Kernel launch bookkeeping: counts every launch and, with timing enabled,
+// brackets it with CUDA events on the context stream.
+void timing_begin(decmg_gpu_ctx* c, int cls, double bytes, cudaEvent_t* a, cudaEvent_t* b);
+void timing_end(decmg_gpu_ctx* c, cudaEvent_t b);
+
+template <class F>
+Status launch(decmg_gpu_ctx* c, int cls, double bytes, F&& f) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (c->timing.enabled) timing_begin(c, cls, bytes, &a, &b);
+    f();
+    ++c->launch_count;
+    if (c->timing.enabled) timing_end(c, b);
+    return cuda_status(cudaGetLastError(), "kernel launch");
+}
+
+inline unsigned grid_for(int64_t threads, int block) {
+    return static_cast<unsigned>((threads + block - 1) / block);
+}
+
+// setup.cu
+Status build_from_base(decmg_gpu_ctx* c, const double* pos, int nv, const int* corners, int nt,
+                       int nsub, unsigned flags);
+Status build_from_levels(decmg_gpu_ctx* c, const decmg_gpu_level_desc* levels, int nlevels,
+                         unsigned flags);
+Status alloc_work(decmg_gpu_ctx* c);
+Status exclusive_scan(decmg_gpu_ctx* c, const int* in, int* out, int n);  // out[n] = total
+
+// cycle.cu
+struct Plan {
+    std::string walk;
+    std::vector<int> pre, post;
+    int smoother = DECMG_SMOOTHER_JACOBI;
+    double omega = 2.0 / 3.0;
+};
+Status make_plan(const decmg_gpu_ctx* c, const decmg_gpu_plan* p, Plan* out);
+Status run_cycles(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b,
+                  const double* d_x0, int ncycles, double* d_x, double* d_hist);
+Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, const double* d_x0,
+             double tol, int max_cycles, double* d_x, double* h_hist, int* cycles_done,
+             double* h_final);
+Status project_compatible(decmg_gpu_ctx* c, int nrhs, double* d_b);
+Status apply_op(decmg_gpu_ctx* c, int level, char op, const double* d_x, double* d_y);
+
+}  // namespace decmg_gpu

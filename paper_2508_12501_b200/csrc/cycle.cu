@@ -1,0 +1,667 @@
+// The V-cycle hot path: smoother, residual, restriction, prolongation +
+// correction, coarse solve, norms, and the cycle driver.
+//
+// Reference path (all in /root/reference/proj):
+//   jacobi_sweep            src/multigrid.cpp:36-56
+//   SparseOperator::apply   src/sparse.cpp:209-218
+//   cycle_once / run_cycle  src/multigrid.cpp:252-323
+//   project_compatible      src/multigrid.cpp:240-250
+//   gmg_solve               src/solvers.cpp:251-279
+//   PinnedDirectSolver      src/direct.cpp:39-76 (stand-in: projected weighted CG)
+//
+// Layout: every vector is [n][nrhs] fp64, so the nrhs values of one vertex
+// are adjacent and a gather of x[col] for a batch is one contiguous segment
+// (128 B for nrhs = 16). Thread mapping: BP (nrhs rounded up to a power of
+// two) consecutive threads own one row, lane = RHS index.
+//
+// Arithmetic: per-row sums start at 0.0 and add v_k * x[c_k] in CSR order,
+// with explicit _rn intrinsics (no FMA), exactly as the reference's CSR loop,
+// so sweeps, residuals and transfers are bit-identical to the reference.
+// Norms and projections use a fixed-shape tree reduction: deterministic run
+// to run, within a few ulps of the reference's blocked sums.
+#include "common.cuh"
+
+#include <algorithm>
+#include <cmath>
+
+namespace decmg_gpu {
+namespace {
+
+constexpr int kBlock = 256;
+
+__device__ __forceinline__ int64_t gtid() {
+    return static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+}
+
+// Fixed-shape block reduction of one value per thread into one partial per
+// lane: rows of the CTA are folded pairwise in a fixed order.
+template <int BP>
+__device__ __forceinline__ void block_partial(double v, double* partial) {
+    __shared__ double sh[kBlock];
+    sh[threadIdx.x] = v;
+    __syncthreads();
+#pragma unroll
+    for (int s = kBlock / 2; s >= BP; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x < BP) partial[static_cast<int64_t>(blockIdx.x) * BP + threadIdx.x] = sh[threadIdx.x];
+}
+
+// jacobi_sweep: s = A x (CSR order), x' = x + (omega (b - s)) / a_ii.
+// x is read entirely before any write (ping-pong buffers), as in the
+// reference, where A.apply fills scratch before the update loop.
+template <int BP>
+__global__ void __launch_bounds__(kBlock) k_sweep(int n, int nrhs, const int* __restrict__ rp,
+                                                  const int* __restrict__ ci,
+                                                  const double* __restrict__ v,
+                                                  const double* __restrict__ x,
+                                                  const double* __restrict__ b,
+                                                  double* __restrict__ xo, double omega) {
+    const int64_t t = gtid();
+    const int64_t row = t / BP;
+    const int lane = static_cast<int>(t % BP);
+    if (row >= n || lane >= nrhs) return;
+    const int k0 = rp[row], k1 = rp[row + 1];
+    double s = 0.0, d = 0.0, xr = 0.0;
+    for (int k = k0; k < k1; ++k) {
+        const int c = ci[k];
+        const double a = v[k];
+        const double xv = x[static_cast<int64_t>(c) * nrhs + lane];
+        s = __dadd_rn(s, __dmul_rn(a, xv));
+        if (c == row) {
+            d = a;
+            xr = xv;
+        }
+    }
+    const int64_t o = row * nrhs + lane;
+    xo[o] = __dadd_rn(xr, __ddiv_rn(__dmul_rn(omega, __dsub_rn(b[o], s)), d));
+}
+
+// First sweep after kernels::fill(0.0, x) (multigrid.cpp:268): A * 0 is
+// exactly +0.0, so x' = 0.0 + (omega (b - 0.0)) / a_ii -- bit-identical to
+// the full sweep without reading the matrix or x.
+template <int BP>
+__global__ void __launch_bounds__(kBlock) k_sweep_zero(int n, int nrhs,
+                                                       const double* __restrict__ diag,
+                                                       const double* __restrict__ b,
+                                                       double* __restrict__ xo, double omega) {
+    const int64_t t = gtid();
+    const int64_t row = t / BP;
+    const int lane = static_cast<int>(t % BP);
+    if (row >= n || lane >= nrhs) return;
+    const int64_t o = row * nrhs + lane;
+    xo[o] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, __dsub_rn(b[o], 0.0)), diag[row]));
+}
+
+// r = b - A x (multigrid.cpp:263-265 / 317-318); optionally stores r and/or
+// emits per-CTA partial sums of r^2 for the residual norm.
+template <int BP, bool STORE>
+__global__ void __launch_bounds__(kBlock) k_residual(int n, int nrhs, const int* __restrict__ rp,
+                                                     const int* __restrict__ ci,
+                                                     const double* __restrict__ v,
+                                                     const double* __restrict__ x,
+                                                     const double* __restrict__ b,
+                                                     double* __restrict__ r,
+                                                     double* __restrict__ partial) {
+    const int64_t t = gtid();
+    const int64_t row = t / BP;
+    const int lane = static_cast<int>(t % BP);
+    const bool valid = row < n && lane < nrhs;
+    double rv = 0.0;
+    if (valid) {
+        const int k0 = rp[row], k1 = rp[row + 1];
+        double s = 0.0;
+        for (int k = k0; k < k1; ++k)
+            s = __dadd_rn(s, __dmul_rn(v[k], x[static_cast<int64_t>(ci[k]) * nrhs + lane]));
+        const int64_t o = row * nrhs + lane;
+        rv = __dsub_rn(b[o], s);
+        if (STORE) r[o] = rv;
+    }
+    if (partial) block_partial<BP>(valid ? __dmul_rn(rv, rv) : 0.0, partial);
+}
+
+// y = A x over CSR rows (SparseOperator::apply); zero_rows: extension x1
+// (coarse RHS cleared on Dirichlet vertices after restriction).
+template <int BP>
+__global__ void __launch_bounds__(kBlock) k_spmv(int nrows, int nrhs, const int* __restrict__ rp,
+                                                 const int* __restrict__ ci,
+                                                 const double* __restrict__ v,
+                                                 const double* __restrict__ x,
+                                                 double* __restrict__ y,
+                                                 const int* __restrict__ zero_rows) {
+    const int64_t t = gtid();
+    const int64_t row = t / BP;
+    const int lane = static_cast<int>(t % BP);
+    if (row >= nrows || lane >= nrhs) return;
+    double s = 0.0;
+    for (int k = rp[row]; k < rp[row + 1]; ++k)
+        s = __dadd_rn(s, __dmul_rn(v[k], x[static_cast<int64_t>(ci[k]) * nrhs + lane]));
+    if (zero_rows && zero_rows[row]) s = 0.0;
+    y[row * nrhs + lane] = s;
+}
+
+// x_f += P x_c (multigrid.cpp:277-280); each fine row owns its entry, so the
+// update is in place.
+template <int BP>
+__global__ void __launch_bounds__(kBlock) k_prolong_add(int n, int nrhs, const int* __restrict__ rp,
+                                                        const int* __restrict__ ci,
+                                                        const double* __restrict__ v,
+                                                        const double* __restrict__ xc,
+                                                        double* __restrict__ xf) {
+    const int64_t t = gtid();
+    const int64_t row = t / BP;
+    const int lane = static_cast<int>(t % BP);
+    if (row >= n || lane >= nrhs) return;
+    double s = 0.0;
+    for (int k = rp[row]; k < rp[row + 1]; ++k)
+        s = __dadd_rn(s, __dmul_rn(v[k], xc[static_cast<int64_t>(ci[k]) * nrhs + lane]));
+    const int64_t o = row * nrhs + lane;
+    xf[o] = __dadd_rn(xf[o], s);
+}
+
+// partials of w_i * b_i (b == nullptr: of w_i) for project_compatible
+template <int BP>
+__global__ void __launch_bounds__(kBlock) k_wsum(int n, int nrhs, const double* __restrict__ w,
+                                                 const double* __restrict__ b,
+                                                 double* __restrict__ partial) {
+    const int64_t t = gtid();
+    const int64_t row = t / BP;
+    const int lane = static_cast<int>(t % BP);
+    const bool valid = row < n && lane < nrhs;
+    double val = 0.0;
+    if (valid) val = b ? __dmul_rn(w[row], b[row * nrhs + lane]) : w[row];
+    block_partial<BP>(val, partial);
+}
+
+// partials of b_i^2
+template <int BP>
+__global__ void __launch_bounds__(kBlock) k_sumsq(int n, int nrhs, const double* __restrict__ b,
+                                                  double* __restrict__ partial) {
+    const int64_t t = gtid();
+    const int64_t row = t / BP;
+    const int lane = static_cast<int>(t % BP);
+    const bool valid = row < n && lane < nrhs;
+    const double val = valid ? b[row * nrhs + lane] : 0.0;
+    block_partial<BP>(__dmul_rn(val, val), partial);
+}
+
+// Second stage: one CTA per lane sums its partials in a fixed order.
+// mode 0: out[lane] = total
+// mode 1: out[lane] = sqrt(total)                      (norm)
+// mode 2: out[lane] = sqrt(total) / denom[lane]         (relative residual)
+__global__ void k_reduce(int nblocks, int BP, const double* __restrict__ partial,
+                         double* __restrict__ out, int mode, const double* __restrict__ denom) {
+    __shared__ double sh[kBlock];
+    const int lane = blockIdx.x;
+    double acc = 0.0;
+    for (int blk = threadIdx.x; blk < nblocks; blk += kBlock)
+        acc = __dadd_rn(acc, partial[static_cast<int64_t>(blk) * BP + lane]);
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = kBlock / 2; s >= 1; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double tot = sh[0];
+        if (mode == 0) out[lane] = tot;
+        else if (mode == 1) out[lane] = __dsqrt_rn(tot);
+        else out[lane] = __ddiv_rn(__dsqrt_rn(tot), denom[lane]);
+    }
+}
+
+__global__ void k_denom(int nrhs, const double* __restrict__ bn, double* __restrict__ denom) {
+    const int l = threadIdx.x;
+    if (l < nrhs) denom[l] = bn[l] > 0.0 ? bn[l] : 1.0;
+}
+
+// b -= (sum w b) / (sum w)   (multigrid.cpp:240-250)
+template <int BP>
+__global__ void __launch_bounds__(kBlock) k_project(int n, int nrhs, const double* __restrict__ num,
+                                                    const double* __restrict__ tot,
+                                                    double* __restrict__ b) {
+    const int64_t t = gtid();
+    const int64_t row = t / BP;
+    const int lane = static_cast<int>(t % BP);
+    if (row >= n || lane >= nrhs) return;
+    const double mean = __ddiv_rn(num[lane], tot[0]);
+    const int64_t o = row * nrhs + lane;
+    b[o] = __dsub_rn(b[o], mean);
+}
+
+// Coarse solve: the projected weighted CG of oracle/ref_standin_direct.cpp,
+// one thread per right-hand side, sequential dots -- bit-identical to the
+// CPU stand-in. Dirichlet (x1): same CG without the two projections.
+__global__ void k_coarse_cg(int n, int nrhs, const int* __restrict__ rp, const int* __restrict__ ci,
+                            const double* __restrict__ v, const double* __restrict__ w, double wtot,
+                            int project, const double* __restrict__ b, double* __restrict__ x,
+                            double* __restrict__ scratch) {
+    const int lane = threadIdx.x;
+    if (lane >= nrhs) return;
+    double* r = scratch + static_cast<int64_t>(lane) * 4 * n;
+    double* p = r + n;
+    double* Ap = p + n;
+    double* xl = Ap + n;
+    if (project) {
+        double m = 0.0;
+        for (int i = 0; i < n; ++i) m = __dadd_rn(m, __dmul_rn(w[i], b[static_cast<int64_t>(i) * nrhs + lane]));
+        m = __ddiv_rn(m, wtot);
+        for (int i = 0; i < n; ++i) r[i] = __dsub_rn(b[static_cast<int64_t>(i) * nrhs + lane], m);
+    } else {
+        for (int i = 0; i < n; ++i) r[i] = b[static_cast<int64_t>(i) * nrhs + lane];
+    }
+    for (int i = 0; i < n; ++i) {
+        xl[i] = 0.0;
+        p[i] = r[i];
+    }
+    double rr = 0.0;
+    for (int i = 0; i < n; ++i) rr = __dadd_rn(rr, __dmul_rn(__dmul_rn(w[i], r[i]), r[i]));
+    const double rr0 = rr;
+    const int maxit = 4 * n + 20;
+    for (int it = 0; it < maxit; ++it) {
+        if (!(rr > __dmul_rn(1e-30, rr0))) break;
+        for (int i = 0; i < n; ++i) {
+            double s = 0.0;
+            for (int k = rp[i]; k < rp[i + 1]; ++k) s = __dadd_rn(s, __dmul_rn(v[k], p[ci[k]]));
+            Ap[i] = s;
+        }
+        double curv = 0.0;
+        for (int i = 0; i < n; ++i) curv = __dadd_rn(curv, __dmul_rn(__dmul_rn(w[i], p[i]), Ap[i]));
+        if (curv == 0.0) break;
+        const double alpha = __ddiv_rn(rr, curv);
+        for (int i = 0; i < n; ++i) xl[i] = __dadd_rn(xl[i], __dmul_rn(alpha, p[i]));
+        for (int i = 0; i < n; ++i) r[i] = __dsub_rn(r[i], __dmul_rn(alpha, Ap[i]));
+        double rn = 0.0;
+        for (int i = 0; i < n; ++i) rn = __dadd_rn(rn, __dmul_rn(__dmul_rn(w[i], r[i]), r[i]));
+        const double beta = __ddiv_rn(rn, rr);
+        for (int i = 0; i < n; ++i) p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
+        rr = rn;
+    }
+    double ym = 0.0;
+    if (project) {
+        for (int i = 0; i < n; ++i) ym = __dadd_rn(ym, __dmul_rn(w[i], xl[i]));
+        ym = __ddiv_rn(ym, wtot);
+    }
+    for (int i = 0; i < n; ++i)
+        x[static_cast<int64_t>(i) * nrhs + lane] = project ? __dsub_rn(xl[i], ym) : xl[i];
+}
+
+// Copy the columns (RHS lanes) selected by mask from src to dst.
+__global__ void k_copy_lanes(int64_t total, int nrhs, unsigned mask, const double* __restrict__ src,
+                             double* __restrict__ dst) {
+    const int64_t t = gtid();
+    if (t >= total) return;
+    const int lane = static_cast<int>(t % nrhs);
+    if (mask & (1u << lane)) dst[t] = src[t];
+}
+
+// ------------------------------------------------------------- dispatch ----
+inline int bp_of(int nrhs) {
+    int bp = 1;
+    while (bp < nrhs) bp *= 2;
+    return bp;
+}
+
+#define DISPATCH_BP(bp, ...)                           \
+    switch (bp) {                                      \
+        case 1: { constexpr int BP = 1; __VA_ARGS__; break; }   \
+        case 2: { constexpr int BP = 2; __VA_ARGS__; break; }   \
+        case 4: { constexpr int BP = 4; __VA_ARGS__; break; }   \
+        case 8: { constexpr int BP = 8; __VA_ARGS__; break; }   \
+        case 16: { constexpr int BP = 16; __VA_ARGS__; break; } \
+        default: { constexpr int BP = 32; __VA_ARGS__; break; } \
+    }
+
+enum Cls { kFineSweep = 0, kFineResidual = 1, kRestrict = 2, kProlong = 3, kCoarseLevels = 4,
+           kCoarseSolve = 5, kNorms = 6 };
+
+struct Driver {
+    decmg_gpu_ctx* c;
+    int nrhs, bp;
+    const double* b0;  // level-0 right-hand side
+
+    const double* bptr(int k) const { return k == 0 ? b0 : c->lv[k].b; }
+    static double* xcur(Level& L) { return L.x[L.cur]; }
+
+    unsigned rows_grid(int n) const { return grid_for(static_cast<int64_t>(n) * bp, kBlock); }
+
+    Status ensure_x(int k) {
+        Level& L = c->lv[k];
+        if (L.x_zero) {
+            DG_CUDA(cudaMemsetAsync(xcur(L), 0, sizeof(double) * L.nv * nrhs, c->stream));
+            L.x_zero = false;
+        }
+        return Status::Ok();
+    }
+
+    Status smooth(int k, int iters, const Plan& plan) {
+        Level& L = c->lv[k];
+        if (iters <= 0) return Status::Ok();
+        if (L.zero_diag_row >= 0)
+            return Status::Err(DECMG_RUNTIME, "jacobi: zero diagonal at row " + std::to_string(L.zero_diag_row));
+        const double R = nrhs;
+        for (int it = 0; it < iters; ++it) {
+            double* xo = L.x[L.cur ^ 1];
+            const double* b = bptr(k);
+            if (L.x_zero) {
+                const double bytes = 8.0 * L.nv + 16.0 * L.nv * R;
+                DG_TRY(launch(c, k == 0 ? kFineSweep : kCoarseLevels, bytes, [&] {
+                    DISPATCH_BP(bp, k_sweep_zero<BP><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+                                        L.nv, nrhs, L.diag, b, xo, plan.omega));
+                }));
+            } else {
+                const double bytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
+                const double* x = xcur(L);
+                DG_TRY(launch(c, k == 0 ? kFineSweep : kCoarseLevels, bytes, [&] {
+                    DISPATCH_BP(bp, k_sweep<BP><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+                                        L.nv, nrhs, L.L_rp, L.L_ci, L.L_v, x, b, xo, plan.omega));
+                }));
+            }
+            L.cur ^= 1;
+            L.x_zero = false;
+        }
+        return Status::Ok();
+    }
+
+    // r = b - A x on level k, then b_{k+1} = R r (multigrid.cpp:263-267)
+    Status residual_restrict(int k) {
+        DG_TRY(ensure_x(k));
+        Level& L = c->lv[k];
+        Level& C = c->lv[k + 1];
+        const double R = nrhs;
+        const double* x = xcur(L);
+        const double* b = bptr(k);
+        const double rbytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
+        DG_TRY(launch(c, k == 0 ? kFineResidual : kCoarseLevels, rbytes, [&] {
+            DISPATCH_BP(bp, (k_residual<BP, true><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+                                L.nv, nrhs, L.L_rp, L.L_ci, L.L_v, x, b, c->r, nullptr)));
+        }));
+        const double tbytes = 12.0 * L.nnzR + 4.0 * (C.nv + 1) + 8.0 * L.nv * R + 8.0 * C.nv * R;
+        const int* zr = c->dirichlet ? C.bd : nullptr;
+        DG_TRY(launch(c, k == 0 ? kRestrict : kCoarseLevels, tbytes, [&] {
+            DISPATCH_BP(bp, k_spmv<BP><<<rows_grid(C.nv), kBlock, 0, c->stream>>>(
+                                C.nv, nrhs, L.R_rp, L.R_ci, L.R_v, c->r, C.b, zr));
+        }));
+        return Status::Ok();
+    }
+
+    // x_k += P_k x_{k+1}
+    Status prolong(int k) {
+        DG_TRY(ensure_x(k));
+        DG_TRY(ensure_x(k + 1));
+        Level& L = c->lv[k];
+        Level& C = c->lv[k + 1];
+        const double R = nrhs;
+        const double bytes = 12.0 * L.nnzP + 4.0 * (L.nv + 1) + 8.0 * C.nv * R + 16.0 * L.nv * R;
+        const double* xc = xcur(C);
+        double* xf = xcur(L);
+        DG_TRY(launch(c, k == 0 ? kProlong : kCoarseLevels, bytes, [&] {
+            DISPATCH_BP(bp, k_prolong_add<BP><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+                                L.nv, nrhs, L.P_rp, L.P_ci, L.P_v, xc, xf));
+        }));
+        return Status::Ok();
+    }
+
+    Status coarse_solve(int k) {
+        Level& L = c->lv[k];
+        double* x = xcur(L);
+        const double* b = bptr(k);
+        const int project = c->dirichlet ? 0 : 1;
+        DG_TRY(launch(c, kCoarseSolve, 0.0, [&] {
+            k_coarse_cg<<<1, 32, 0, c->stream>>>(L.nv, nrhs, L.L_rp, L.L_ci, L.L_v, L.area, L.wtot,
+                                                 project, b, x, c->coarse_scratch);
+        }));
+        L.x_zero = false;
+        return Status::Ok();
+    }
+
+    // MultigridHierarchy::cycle_once (multigrid.cpp:252-285)
+    Status cycle_once(const Plan& plan) {
+        const int nw = static_cast<int>(plan.walk.size());
+        const int Lc = static_cast<int>(c->lv.size());
+        int level = 0;
+        for (int w = 0; w < nw; ++w) {
+            if (plan.walk[w] == 'd') {
+                DG_TRY(smooth(level, plan.pre[level], plan));
+                DG_TRY(residual_restrict(level));
+                ++level;
+                c->lv[level].x_zero = true;  // kernels::fill(0.0, xs[level])
+                if (level == Lc - 1) {
+                    DG_TRY(coarse_solve(level));
+                } else if (w + 1 < nw && plan.walk[w + 1] == 'u') {
+                    DG_TRY(smooth(level, plan.pre[level], plan));
+                }
+            } else {
+                DG_TRY(prolong(level - 1));
+                --level;
+                DG_TRY(smooth(level, plan.post[level], plan));
+            }
+        }
+        return Status::Ok();
+    }
+
+    int partial_blocks(int n) const { return static_cast<int>(rows_grid(n)); }
+
+    // out[lane] = ||b||_2 over level-0 rows of vector v (mode 1) or sum (0)
+    Status sumsq(const double* v, double* out, int mode) {
+        const int n = c->lv[0].nv;
+        DG_TRY(launch(c, kNorms, 8.0 * n * nrhs, [&] {
+            DISPATCH_BP(bp, k_sumsq<BP><<<rows_grid(n), kBlock, 0, c->stream>>>(n, nrhs, v, c->red));
+        }));
+        DG_TRY(launch(c, kNorms, 0.0, [&] {
+            k_reduce<<<nrhs, kBlock, 0, c->stream>>>(partial_blocks(n), bp, c->red, out, mode, nullptr);
+        }));
+        return Status::Ok();
+    }
+
+    // hist[lane] = ||b - A x||_2 / denom[lane] on level 0 (multigrid.cpp:317-319)
+    Status resnorm(double* hist, const double* denom) {
+        DG_TRY(ensure_x(0));
+        Level& L = c->lv[0];
+        const double* x = xcur(L);
+        const double bytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 16.0 * L.nv * nrhs;
+        DG_TRY(launch(c, kFineResidual, bytes, [&] {
+            DISPATCH_BP(bp, (k_residual<BP, false><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+                                L.nv, nrhs, L.L_rp, L.L_ci, L.L_v, x, b0, nullptr, c->red)));
+        }));
+        DG_TRY(launch(c, kNorms, 0.0, [&] {
+            k_reduce<<<nrhs, kBlock, 0, c->stream>>>(partial_blocks(L.nv), bp, c->red, hist, 2, denom);
+        }));
+        return Status::Ok();
+    }
+
+    // denom[lane] = ||b|| > 0 ? ||b|| : 1   (multigrid.cpp:307-308)
+    Status make_denom(double* denom) {
+        double* bn = c->dsmall + 64;
+        DG_TRY(sumsq(b0, bn, 1));
+        DG_TRY(launch(c, kNorms, 0.0, [&] { k_denom<<<1, 32, 0, c->stream>>>(nrhs, bn, denom); }));
+        return Status::Ok();
+    }
+
+    Status one_cycle(const Plan& plan) {
+        if (c->lv.size() == 1) return coarse_solve(0);
+        return cycle_once(plan);
+    }
+
+    Status load_x0(const double* d_x0) {
+        Level& L = c->lv[0];
+        if (d_x0) {
+            DG_CUDA(cudaMemcpyAsync(xcur(L), d_x0, sizeof(double) * L.nv * nrhs, cudaMemcpyDeviceToDevice,
+                                    c->stream));
+            L.x_zero = false;
+        } else {
+            L.x_zero = true;
+        }
+        return Status::Ok();
+    }
+};
+
+Status check_nrhs(const decmg_gpu_ctx* c, int nrhs) {
+    if (nrhs < 1 || nrhs > c->max_nrhs || nrhs > 32)
+        return Status::Err(DECMG_INVALID_ARGUMENT, "nrhs must be in [1, max_nrhs] (max 32)");
+    return Status::Ok();
+}
+
+}  // namespace
+
+Status make_plan(const decmg_gpu_ctx* c, const decmg_gpu_plan* p, Plan* out) {
+    const int L = static_cast<int>(c->lv.size());
+    Plan q;
+    if (p && p->smoother != DECMG_SMOOTHER_JACOBI)
+        return Status::Err(DECMG_INVALID_ARGUMENT, "smoother: only weighted Jacobi is implemented on the device");
+    q.omega = p ? p->jacobi_omega : 2.0 / 3.0;
+    if (p && p->walk) {
+        q.walk = p->walk;
+    } else {
+        for (int i = 0; i < L - 1; ++i) q.walk.push_back('d');
+        for (int i = 0; i < L - 1; ++i) q.walk.push_back('u');
+    }
+    for (int k = 0; k < L; ++k) {
+        q.pre.push_back(p ? (p->pre ? p->pre[k] : p->pre_all) : 2);
+        q.post.push_back(p ? (p->post ? p->post[k] : p->post_all) : 2);
+    }
+    // CyclePlan::validate (multigrid.cpp:131-143)
+    int level = 0;
+    for (char t : q.walk) {
+        if (t != 'd' && t != 'u') return Status::Err(DECMG_INVALID_ARGUMENT, "CyclePlan: walk must be 'd'/'u'");
+        level += t == 'd' ? 1 : -1;
+        if (level < 0) return Status::Err(DECMG_INVALID_ARGUMENT, "CyclePlan: walk rises above the finest level");
+        if (level > L - 1)
+            return Status::Err(DECMG_INVALID_ARGUMENT, "CyclePlan: walk descends below the coarsest level");
+    }
+    if (level != 0) return Status::Err(DECMG_INVALID_ARGUMENT, "CyclePlan: walk does not return to the finest level");
+    *out = std::move(q);
+    return Status::Ok();
+}
+
+Status run_cycles(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, const double* d_x0,
+                  int ncycles, double* d_x, double* d_hist) {
+    DG_TRY(check_nrhs(c, nrhs));
+    if (ncycles < 0) return Status::Err(DECMG_INVALID_ARGUMENT, "CyclePlan: negative cycle count");
+    Driver dr{c, nrhs, bp_of(nrhs), d_b};
+    double* denom = c->dsmall;
+    DG_TRY(dr.load_x0(d_x0));
+    DG_TRY(dr.make_denom(denom));
+    for (int cyc = 0; cyc < ncycles; ++cyc) {
+        DG_TRY(dr.one_cycle(plan));
+        DG_TRY(dr.resnorm(d_hist + static_cast<int64_t>(cyc) * nrhs, denom));
+    }
+    DG_TRY(dr.ensure_x(0));
+    Level& L = c->lv[0];
+    DG_CUDA(cudaMemcpyAsync(d_x, L.x[L.cur], sizeof(double) * L.nv * nrhs, cudaMemcpyDeviceToDevice, c->stream));
+    return Status::Ok();
+}
+
+Status project_compatible(decmg_gpu_ctx* c, int nrhs, double* d_b) {
+    DG_TRY(check_nrhs(c, nrhs));
+    const int bp = bp_of(nrhs);
+    const Level& L = c->lv[0];
+    double* num = c->dsmall + 128;
+    double* tot = c->dsmall + 192;
+    const unsigned g = grid_for(static_cast<int64_t>(L.nv) * bp, kBlock);
+    DG_TRY(launch(c, kNorms, 16.0 * L.nv * nrhs, [&] {
+        DISPATCH_BP(bp, k_wsum<BP><<<g, kBlock, 0, c->stream>>>(L.nv, nrhs, L.area, d_b, c->red));
+    }));
+    DG_TRY(launch(c, kNorms, 0.0, [&] { k_reduce<<<nrhs, kBlock, 0, c->stream>>>(g, bp, c->red, num, 0, nullptr); }));
+    const unsigned g1 = grid_for(L.nv, kBlock);
+    DG_TRY(launch(c, kNorms, 8.0 * L.nv, [&] {
+        k_wsum<1><<<g1, kBlock, 0, c->stream>>>(L.nv, 1, L.area, nullptr, c->red);
+    }));
+    DG_TRY(launch(c, kNorms, 0.0, [&] { k_reduce<<<1, kBlock, 0, c->stream>>>(g1, 1, c->red, tot, 0, nullptr); }));
+    DG_TRY(launch(c, kNorms, 16.0 * L.nv * nrhs, [&] {
+        DISPATCH_BP(bp, k_project<BP><<<g, kBlock, 0, c->stream>>>(L.nv, nrhs, num, tot, d_b));
+    }));
+    return Status::Ok();
+}
+
+// gmg_solve (proj/src/solvers.cpp:251-279), batched: each RHS stops at its
+// own cycle count; its solution is the iterate of that cycle.
+Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, const double* d_x0,
+             double tol, int max_cycles, double* d_x, double* h_hist, int* cycles_done,
+             double* h_final) {
+    DG_TRY(check_nrhs(c, nrhs));
+    if (max_cycles < 0) return Status::Err(DECMG_INVALID_ARGUMENT, "gmg_solve: max_cycles >= 0");
+    Level& L0 = c->lv[0];
+    const size_t nbytes = sizeof(double) * L0.nv * nrhs;
+    DG_CUDA(cudaMemcpyAsync(c->bproj, d_b, nbytes, cudaMemcpyDeviceToDevice, c->stream));
+    if (!c->dirichlet) DG_TRY(project_compatible(c, nrhs, c->bproj));
+    Driver dr{c, nrhs, bp_of(nrhs), c->bproj};
+    double* denom = c->dsmall;
+    double* dres = c->dsmall + 256;
+    DG_TRY(dr.load_x0(d_x0));
+    DG_TRY(dr.make_denom(denom));
+    std::vector<int> done(nrhs, 0);
+    std::vector<double> final_res(nrhs, 0.0);
+    const unsigned all = nrhs == 32 ? 0xffffffffu : ((1u << nrhs) - 1u);
+    unsigned active = all;
+    const int64_t total = static_cast<int64_t>(L0.nv) * nrhs;
+    int cyc = 0;
+    if (max_cycles == 0) {
+        DG_TRY(dr.resnorm(dres, denom));
+        DG_CUDA(cudaMemcpyAsync(c->hsmall, dres, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, c->stream));
+        DG_CUDA(cudaStreamSynchronize(c->stream));
+        for (int l = 0; l < nrhs; ++l) final_res[l] = c->hsmall[l];
+    }
+    while (cyc < max_cycles && active) {
+        DG_TRY(dr.one_cycle(plan));
+        DG_TRY(dr.resnorm(dres, denom));
+        DG_CUDA(cudaMemcpyAsync(c->hsmall, dres, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, c->stream));
+        DG_CUDA(cudaStreamSynchronize(c->stream));
+        ++cyc;
+        unsigned fin = 0;
+        for (int l = 0; l < nrhs; ++l) {
+            if (!(active & (1u << l))) continue;
+            const double res = c->hsmall[l];
+            if (h_hist) h_hist[static_cast<int64_t>(cyc - 1) * nrhs + l] = res;
+            final_res[l] = res;
+            done[l] = cyc;
+            if (res <= tol || cyc == max_cycles) fin |= 1u << l;
+        }
+        if (fin) {
+            DG_TRY(dr.ensure_x(0));
+            const double* src = L0.x[L0.cur];
+            DG_TRY(launch(c, kNorms, 16.0 * L0.nv * nrhs, [&] {
+                k_copy_lanes<<<grid_for(total, kBlock), kBlock, 0, c->stream>>>(total, nrhs, fin, src, c->xsol);
+            }));
+            active &= ~fin;
+        }
+    }
+    if (active) {  // max_cycles == 0: the solution is x0
+        DG_TRY(dr.ensure_x(0));
+        const double* src = L0.x[L0.cur];
+        DG_TRY(launch(c, kNorms, 16.0 * L0.nv * nrhs, [&] {
+            k_copy_lanes<<<grid_for(total, kBlock), kBlock, 0, c->stream>>>(total, nrhs, active, src, c->xsol);
+        }));
+    }
+    DG_CUDA(cudaMemcpyAsync(d_x, c->xsol, nbytes, cudaMemcpyDeviceToDevice, c->stream));
+    DG_CUDA(cudaStreamSynchronize(c->stream));
+    for (int l = 0; l < nrhs; ++l) {
+        if (cycles_done) cycles_done[l] = done[l];
+        if (h_final) h_final[l] = final_res[l];
+    }
+    return Status::Ok();
+}
+
+Status apply_op(decmg_gpu_ctx* c, int level, char op, const double* d_x, double* d_y) {
+    const int L = static_cast<int>(c->lv.size());
+    if (level < 0 || level >= L) return Status::Err(DECMG_INVALID_ARGUMENT, "apply: level out of range");
+    Level& m = c->lv[level];
+    const int *rp, *ci;
+    const double* v;
+    int rows;
+    if (op == 'L') {
+        rp = m.L_rp; ci = m.L_ci; v = m.L_v; rows = m.nv;
+    } else if ((op == 'P' || op == 'R') && level + 1 < L) {
+        if (op == 'P') { rp = m.P_rp; ci = m.P_ci; v = m.P_v; rows = m.nv; }
+        else { rp = m.R_rp; ci = m.R_ci; v = m.R_v; rows = c->lv[level + 1].nv; }
+    } else {
+        return Status::Err(DECMG_INVALID_ARGUMENT, "apply: unknown operator for this level");
+    }
+    DG_TRY(launch(c, kNorms, 0.0, [&] {
+        k_spmv<1><<<grid_for(rows, kBlock), kBlock, 0, c->stream>>>(rows, 1, rp, ci, v, d_x, d_y, nullptr);
+    }));
+    return Status::Ok();
+}
+
+}  // namespace decmg_gpu

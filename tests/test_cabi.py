@@ -1,0 +1,108 @@
+"""CPU checks of the C-ABI library and the host-side mirror (no GPU needed).
+
+- libdecmg_gpu.so loads and exports every symbol include/decmg_gpu.h declares;
+- the C++ shim include/decmg_gpu.hpp compiles against the C header;
+- host-only entry points (base-mesh generators) agree with the oracle;
+- cycle plans reproduce the reference's walks (proj/tests/test_multigrid.cpp:77-111).
+"""
+import re
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2508_12501_b200 as d
+from paper_2508_12501_b200 import _lib
+from oracle_ctypes import OracleHierarchy
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "decmg_gpu.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"DECMG_API\s+[\w\s\*]+?\b(decmg_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    syms = declared_symbols()
+    assert len(syms) >= 19
+    lib = _lib.load()
+    for s in syms:
+        assert hasattr(lib, s), s
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True, text=True,
+                         check=True).stdout
+    exported = set(re.findall(r"\bT (decmg_\w+)", out))
+    assert set(syms) <= exported
+    assert set(_lib.SIGNATURES) == set(syms), "ctypes signature table out of sync with the header"
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_cpp_shim_compiles():
+    shim = ROOT / "include" / "decmg_gpu.hpp"
+    src = '#include "decmg_gpu.hpp"\nint main(){ auto p = decmg::standard_plan(3, decmg::CycleKind::W); return p.walk.size() == 6 ? 0 : 1; }\n'
+    exe = ROOT / "build" / "shim_test"
+    exe.parent.mkdir(exist_ok=True)
+    (exe.parent / "shim_test.cpp").write_text(src)
+    subprocess.run(["g++", "-std=c++17", "-I", str(shim.parent), str(exe.parent / "shim_test.cpp"), "-o", str(exe),
+                    "-L", str(_lib.LIB_PATH.parent), "-ldecmg_gpu", f"-Wl,-rpath,{_lib.LIB_PATH.parent}"],
+                   check=True)
+    assert subprocess.run([str(exe)]).returncode == 0
+
+
+@pytest.mark.parametrize("spec", ["square", "ico", "grid:3:2:2.0:1.5", "equi:4:8:1.0"])
+def test_base_meshes_match_oracle(spec):
+    pos, tri = d.base_mesh(spec)
+    o = OracleHierarchy(spec, 0)
+    np.testing.assert_array_equal(pos.ravel(), o.get(0, "positions"))
+    # corner triples -> the oracle's edge triples through from_triangles
+    assert tri.shape[0] == o.info(0)["nt"]
+
+
+def test_ico_faces_outward():
+    pos, tri = d.base_mesh("ico")
+    for a, b, c in tri:
+        n = np.cross(pos[b] - pos[a], pos[c] - pos[a])
+        assert np.dot(n, pos[a]) > 0
+
+
+def test_standard_plans_match_reference_walks():
+    w = lambda s: [d.Transition.Down if ch == "d" else d.Transition.Up for ch in s]
+    assert d.standard_plan(2, d.CycleKind.V).walk == w("du")
+    assert d.standard_plan(3, d.CycleKind.V).walk == w("dduu")
+    assert d.standard_plan(3, d.CycleKind.W).walk == w("dduduu")
+    assert d.standard_plan(3, d.CycleKind.F).walk == w("dduduu")
+    for levels in range(1, 6):
+        for kind in d.CycleKind:
+            p = d.standard_plan(levels, kind)
+            p.validate(levels)
+            if levels > 1:
+                assert p.depth() == levels
+    w4 = d.standard_plan(4, d.CycleKind.W)
+    level, visits = 0, 0
+    for t in w4.walk:
+        level += 1 if t == d.Transition.Down else -1
+        visits += level == 3
+    assert visits == 4
+
+
+def test_plan_validation_rejects_bad_walks():
+    p = d.CyclePlan(pre=[3] * 3, post=[3] * 3)
+    for bad in ("ddu", "ud", "dddu"):
+        p.walk = [d.Transition.Down if ch == "d" else d.Transition.Up for ch in bad]
+        with pytest.raises(ValueError):
+            p.validate(3)
+    p.walk = [d.Transition.Down, d.Transition.Up]
+    p.validate(3)
+
+
+def test_no_cpu_fallback_when_library_missing(tmp_path, monkeypatch):
+    monkeypatch.setattr(_lib, "LIB_PATH", tmp_path / "missing.so")
+    monkeypatch.setattr(_lib, "_lib", None)
+    with pytest.raises(ImportError, match="no CPU fallback"):
+        _lib.load()

@@ -1,0 +1,279 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference goldens
+and the CPU oracle.
+
+Bars (BASELINE.json north_star): bit-exact integer mesh/connectivity/sparsity;
+per-cycle residual norms within 1e-10 relative; same cycle count to 1e-8
+(within 1). In addition every row-local kernel (sweep, residual, restriction,
+prolongation, SpMV, coarse CG) is bit-identical to the reference, so iterates
+from run_cycle on an identical right-hand side must match bit for bit.
+"""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2508_12501_b200 as d
+from oracle_ctypes import OracleHierarchy, fnv
+
+pytestmark = pytest.mark.gpu
+GOLDEN = Path(__file__).resolve().parent / "golden"
+RTOL_HIST = 1e-10
+
+
+def load(stem):
+    return json.loads((GOLDEN / f"{stem}.json").read_text())
+
+
+def gpu_from_argv(argv, max_nrhs=1):
+    base, k, bc = argv[1], int(argv[2]), argv[3]
+    return d.MultigridHierarchy.from_base(base, k, dirichlet=(bc == "dirichlet"), max_nrhs=max_nrhs)
+
+
+EXPORT = {"L": ("L_row_ptr", "L_col_idx", "L_values"), "P": ("P_row_ptr", "P_col_idx", "P_values"),
+          "R": ("R_row_ptr", "R_col_idx", "R_values")}
+
+
+@pytest.mark.parametrize("stem", sorted(p.stem for p in GOLDEN.glob("struct_*.json")))
+def test_structure_bit_exact_vs_reference(stem):
+    """Mesh hash, edges, triangles, positions, dual areas and the CSR arrays of
+    L, P, R built on the device equal the reference's (proj/src/mesh.cpp:112-119,
+    operators.cpp:102-122, geometric_map.cpp:205-223)."""
+    g = load(stem)
+    h = gpu_from_argv(g["_argv"])
+    assert h.levels() == len(g["levels"])
+    for k, lv in enumerate(g["levels"]):
+        info = h.level_info(k)
+        assert (info["nv"], info["ne"], info["nt"]) == (lv["nv"], lv["ne"], lv["nt"])
+        assert str(h.mesh_hash(k)) == lv["hash"]
+        assert str(fnv(h.export(k, "edges"))) == lv["fnv_edges"]
+        assert str(fnv(h.export(k, "triangles"))) == lv["fnv_triangles"]
+        assert str(fnv(h.export(k, "positions"))) == lv["fnv_positions"]
+        assert str(fnv(h.export(k, "dual_areas"))) == lv["fnv_dual_areas"]
+        for key in ["L"] + (["P", "R"] if "P" in lv else []):
+            rp, ci, v = (h.export(k, n) for n in EXPORT[key])
+            assert str(fnv(rp)) == lv[key]["fnv_row_ptr"], (key, k)
+            assert str(fnv(ci)) == lv[key]["fnv_col_idx"], (key, k)
+            if "values" in lv[key]:
+                np.testing.assert_array_equal(v, np.array(lv[key]["values"]))
+            assert str(fnv(v)) == lv[key]["fnv_values"], (key, k)
+
+
+@pytest.mark.parametrize("base,nsub,dirichlet", [("ico", 7, False), ("square", 7, True), ("equi:4:8:1.0", 4, False)])
+def test_structure_bit_exact_vs_oracle(base, nsub, dirichlet):
+    h = d.MultigridHierarchy.from_base(base, nsub, dirichlet=dirichlet)
+    o = OracleHierarchy(base, nsub, dirichlet)
+    for k in range(h.levels()):
+        assert h.mesh_hash(k) == o.info(k)["hash"]
+        for ours, theirs in [("edges", "edges"), ("triangles", "triangles"), ("positions", "positions"),
+                             ("dual_areas", "dual_areas"), ("boundary", "boundary"), ("L_row_ptr", "L_rp"),
+                             ("L_col_idx", "L_ci"), ("L_values", "L_v")]:
+            np.testing.assert_array_equal(h.export(k, ours), o.get(k, theirs), err_msg=f"{ours} level {k}")
+        if k + 1 < h.levels():
+            for ours, theirs in [("P_row_ptr", "P_rp"), ("P_col_idx", "P_ci"), ("P_values", "P_v"),
+                                 ("R_row_ptr", "R_rp"), ("R_col_idx", "R_ci"), ("R_values", "R_v")]:
+                np.testing.assert_array_equal(h.export(k, ours), o.get(k, theirs), err_msg=f"{ours} level {k}")
+
+
+def test_spmv_bitwise_equal_to_reference_apply():
+    """Mirrors proj/tests/test_kernels.cpp:99-111 (CSR SpMV bitwise-equal)."""
+    h = d.MultigridHierarchy.from_base("ico", 6)
+    o = OracleHierarchy("ico", 6)
+    rng = np.random.default_rng(7)
+    for k in range(h.levels()):
+        x = rng.random(h.n(k))
+        np.testing.assert_array_equal(h.apply(k, "L", x), o.spmv(k, "L", x))
+        if k + 1 < h.levels():
+            xc = rng.random(h.n(k + 1))
+            np.testing.assert_array_equal(h.apply(k, "P", xc), o.spmv(k, "P", xc))
+            np.testing.assert_array_equal(h.apply(k, "R", x), o.spmv(k, "R", x))
+
+
+@pytest.mark.parametrize("stem", sorted(p.stem for p in GOLDEN.glob("cycles_*.json") if not p.stem.endswith("_gs")))
+def test_run_cycle_iterates_bitwise_vs_reference(stem):
+    """run_cycle (multigrid.cpp:287-323) from the reference's own projected RHS:
+    bit-identical iterate, residual history within 1e-10 relative."""
+    g = load(stem)
+    argv = g["_argv"]
+    h = gpu_from_argv(argv)
+    o = OracleHierarchy(argv[1], int(argv[2]), argv[3] == "dirichlet")
+    b = o.rhs(argv[4], int(argv[5]))
+    if argv[3] != "dirichlet":
+        b = o.project(b)
+    assert str(fnv(b)) == g["fnv_b"]
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan.cycles = int(argv[6])
+    res = h.run_cycle(plan, b, np.zeros_like(b))
+    ref = np.array(g["history"])
+    assert np.all(np.abs(res.residual_history - ref) <= RTOL_HIST * np.abs(ref))
+    assert str(fnv(res.x)) == g["fnv_x"], "iterate not bit-identical to the reference"
+
+
+@pytest.mark.parametrize("stem", ["solve_config1", "solve_config2", "solve_config3", "solve_equi_4_8_3_lr",
+                                  "solve_square_6_uniform"])
+def test_gmg_solve_vs_reference(stem):
+    """gmg_solve (solvers.cpp:251-279): same cycle count to tol, per-cycle
+    residuals within 1e-10 relative (BASELINE configs 1-3)."""
+    g = load(stem)
+    argv = g["_argv"]
+    h = gpu_from_argv(argv)
+    kind, seed, tol, maxc = argv[4], int(argv[5]), float(argv[6]), int(argv[7])
+    b = h.make_rhs(kind, seed)
+    o = OracleHierarchy(argv[1], int(argv[2]), argv[3] == "dirichlet")
+    np.testing.assert_array_equal(b, o.rhs(kind, seed))
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    rep = d.gmg_solve(h, plan, b, tol, maxc)
+    ref = np.array(g["history"])
+    assert abs(rep.iterations - g["iterations"]) <= 1
+    m = min(len(ref), rep.iterations)
+    hist = np.array(rep.residual_history[:m])
+    assert np.all(np.abs(hist - ref[:m]) <= RTOL_HIST * np.abs(ref[:m])), (hist, ref)
+    assert rep.converged
+
+
+def test_batched_rhs_match_single_rhs_oracle():
+    """16 right-hand sides in one [n][16] batch (config 4 layout) give each
+    RHS's single-vector reference history and iterate."""
+    base, nsub, nrhs = "ico", 5, 16
+    h = d.MultigridHierarchy.from_base(base, nsub, max_nrhs=nrhs)
+    o = OracleHierarchy(base, nsub)
+    B = h.make_rhs("uniform", 100, nrhs)
+    Bp = np.stack([o.project(B[:, j]) for j in range(nrhs)], axis=1)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan.cycles = 6
+    res = h.run_cycle(plan, Bp, np.zeros_like(Bp))
+    for j in range(nrhs):
+        ox, oh = o.run_cycles(Bp[:, j], ncycles=6)
+        np.testing.assert_array_equal(res.x[:, j], ox)
+        assert np.all(np.abs(res.residual_history[:, j] - oh) <= RTOL_HIST * oh)
+    rep = d.gmg_solve(h, d.standard_plan(h.levels(), d.CycleKind.V, 2, 2), B, 1e-8, 100)
+    for j in range(nrhs):
+        ox, oh, oit, _ = o.solve(B[:, j], tol=1e-8, max_cycles=100)
+        assert abs(rep.iterations[j] - oit) <= 1
+        m = min(oit, rep.iterations[j])
+        assert np.all(np.abs(np.array(rep.residual_history[j][:m]) - oh[:m]) <= RTOL_HIST * oh[:m])
+
+
+def test_w_and_f_walks_bitwise():
+    h = d.MultigridHierarchy.from_base("equi:4:8:1.0", 3)
+    o = OracleHierarchy("equi:4:8:1.0", 3)
+    b = o.project(o.rhs("lr", 11))
+    for kind in (d.CycleKind.W, d.CycleKind.F):
+        plan = d.standard_plan(h.levels(), kind, 2, 2)
+        plan.cycles = 4
+        res = h.run_cycle(plan, b)
+        ox, oh = o.run_cycles(b, ncycles=4, walk=plan.walk_string())
+        np.testing.assert_array_equal(res.x, ox)
+        assert np.all(np.abs(res.residual_history - oh) <= RTOL_HIST * oh)
+    # truncated walk that bottoms out above the coarsest level (multigrid.cpp:271-275)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan.walk = [d.Transition.Down, d.Transition.Down, d.Transition.Up, d.Transition.Up]
+    plan.cycles = 3
+    res = h.run_cycle(plan, b)
+    ox, oh = o.run_cycles(b, ncycles=3, walk="dduu")
+    np.testing.assert_array_equal(res.x, ox)
+
+
+def test_reference_unit_semantics():
+    """Mirrors proj/tests/test_multigrid.cpp: hierarchy shapes (113-131),
+    transfers preserve constants (133-149), zero data stays zero (151-164),
+    contraction <= 0.5 per cycle for 5 seeds (195-212), bit-identical reruns
+    (214-227), one-level hierarchy = coarse solve (183-193)."""
+    h = d.MultigridHierarchy.from_base("equi:4:8:1.0", 3)
+    assert [h.n(k) for k in range(4)] == [1089, 289, 81, 25]
+    for k in range(3):
+        np.testing.assert_allclose(h.apply(k, "P", np.ones(h.n(k + 1))), 1.0, rtol=1e-12)
+        np.testing.assert_allclose(h.apply(k, "R", np.ones(h.n(k))), 1.0, rtol=1e-12)
+    for k in range(4):
+        lap = h.apply(k, "L", np.ones(h.n(k)))
+        assert np.max(np.abs(lap)) <= 1e-12 * np.max(np.abs(h.export(k, "L_values")))
+    plan = d.standard_plan(4, d.CycleKind.V, 2, 2)
+    plan.cycles = 3
+    z = np.zeros(h.n())
+    res = h.run_cycle(plan, z, z)
+    assert np.all(res.x == 0.0) and np.all(res.residual_history == 0.0)
+    plan.cycles = 10
+    for seed in range(1, 6):
+        b = h.project_compatible(h.make_rhs("lr", seed))
+        r = h.run_cycle(plan, b).residual_history
+        for k in range(len(r) - 1):
+            if r[k] > 1e-10:
+                assert r[k + 1] <= 0.5 * r[k]
+        assert r[-1] <= 1e-6
+        r2 = h.run_cycle(plan, b).residual_history
+        np.testing.assert_array_equal(r, r2)
+    one = d.MultigridHierarchy.from_base("equi:4:8:1.0", 0)
+    b = one.project_compatible(one.make_rhs("lr", 5))
+    p1 = d.standard_plan(1, d.CycleKind.V)
+    r = one.run_cycle(p1, b, np.zeros_like(b)).residual_history
+    assert r[-1] <= 1e-12
+
+
+def test_errors_surface_like_the_reference():
+    h = d.MultigridHierarchy.from_base("square", 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V)
+    bad = d.CyclePlan(walk=[d.Transition.Down, d.Transition.Down, d.Transition.Up], pre=[1] * 3, post=[1] * 3)
+    with pytest.raises(ValueError, match="does not return"):
+        h.run_cycle(bad, np.zeros(h.n()))
+    with pytest.raises(ValueError, match="size mismatch"):
+        h.run_cycle(plan, np.zeros(h.n() + 1))
+    # zero diagonal -> runtime_error "jacobi: zero diagonal at row i" (multigrid.cpp:47-51)
+    lv = [dict(nv=2, L_row_ptr=[0, 1, 2], L_col_idx=[0, 1], L_values=[1.0, 0.0], dual_areas=[1.0, 1.0])]
+    lv2 = [dict(nv=2, L_row_ptr=[0, 1, 2], L_col_idx=[0, 1], L_values=[1.0, 0.0], dual_areas=[1.0, 1.0],
+                P_row_ptr=[0, 1, 2], P_col_idx=[0, 0], P_values=[1.0, 1.0], R_row_ptr=[0, 2],
+                R_col_idx=[0, 1], R_values=[0.5, 0.5]),
+           dict(nv=1, L_row_ptr=[0, 1], L_col_idx=[0], L_values=[1.0], dual_areas=[1.0])]
+    hz = d.MultigridHierarchy.from_levels(lv2)
+    with pytest.raises(RuntimeError, match="jacobi: zero diagonal at row 1"):
+        hz.run_cycle(d.standard_plan(2, d.CycleKind.V, 1, 1), np.ones(2))
+    assert d.MultigridHierarchy.from_levels(lv).levels() == 1
+    with pytest.raises(RuntimeError, match="bad corner triple"):
+        d.MultigridHierarchy.from_base((np.zeros((3, 3)), np.array([[0, 1, 1]])), 1)
+
+
+def test_from_levels_matches_from_base():
+    """create_from_levels (host-assembled reference layout) runs the same cycles."""
+    o = OracleHierarchy("ico", 4)
+    levels = []
+    for k in range(o.levels):
+        lv = dict(nv=o.n(k), L_row_ptr=o.get(k, "L_rp"), L_col_idx=o.get(k, "L_ci"), L_values=o.get(k, "L_v"),
+                  dual_areas=o.get(k, "dual_areas"))
+        if k + 1 < o.levels:
+            lv.update(P_row_ptr=o.get(k, "P_rp"), P_col_idx=o.get(k, "P_ci"), P_values=o.get(k, "P_v"),
+                      R_row_ptr=o.get(k, "R_rp"), R_col_idx=o.get(k, "R_ci"), R_values=o.get(k, "R_v"))
+        levels.append(lv)
+    h = d.MultigridHierarchy.from_levels(levels)
+    b = o.project(o.rhs("uniform", 3))
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan.cycles = 5
+    res = h.run_cycle(plan, b)
+    ox, oh = o.run_cycles(b, ncycles=5)
+    np.testing.assert_array_equal(res.x, ox)
+
+
+@pytest.mark.parametrize("nsub", [10])
+def test_config4_full_size(nsub):
+    """BASELINE config 4 (icosphere x10, 10,485,762 vertices, 16 RHS) at full
+    size: structure counts and hashes against the oracle on the finest level,
+    bit-identical first RHS iterate after 2 batched cycles, and
+    size-independent properties (L 1 = 0, contraction per cycle)."""
+    nrhs = 16
+    h = d.MultigridHierarchy.from_base("ico", nsub, max_nrhs=nrhs)
+    assert h.n() == 10 * 4 ** nsub + 2
+    info = h.level_info(0)
+    assert info["nnz_L"] == 70 * 4 ** nsub + 2
+    o = OracleHierarchy("ico", nsub)
+    assert h.mesh_hash(0) == o.info(0)["hash"]
+    assert fnv(h.export(0, "L_values")) == fnv(o.get(0, "L_v"))
+    B = h.make_rhs("uniform", 1, nrhs)
+    B0 = o.project(B[:, 0])
+    Bp = h.project_compatible(B)
+    np.testing.assert_allclose(Bp[:, 0], B0, rtol=0, atol=1e-15)
+    Bp[:, 0] = B0
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan.cycles = 2
+    res = h.run_cycle(plan, Bp)
+    ox, oh = o.run_cycles(B0, ncycles=2)
+    np.testing.assert_array_equal(res.x[:, 0], ox)
+    assert np.all(np.abs(res.residual_history[:, 0] - oh) <= RTOL_HIST * oh)
+    assert np.all(res.residual_history[1] < 0.5 * res.residual_history[0])
