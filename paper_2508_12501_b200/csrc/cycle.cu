@@ -160,20 +160,6 @@ __global__ void __launch_bounds__(kBlock) k_prolong_add(int n, int nrhs, const i
     xf[o] = __dadd_rn(xf[o], s);
 }
 
-// partials of w_i * b_i (b == nullptr: of w_i) for project_compatible
-template <int BP>
-__global__ void __launch_bounds__(kBlock) k_wsum(int n, int nrhs, const double* __restrict__ w,
-                                                 const double* __restrict__ b,
-                                                 double* __restrict__ partial) {
-    const int64_t t = gtid();
-    const int64_t row = t / BP;
-    const int lane = static_cast<int>(t % BP);
-    const bool valid = row < n && lane < nrhs;
-    double val = 0.0;
-    if (valid) val = b ? __dmul_rn(w[row], b[row * nrhs + lane]) : w[row];
-    block_partial<BP>(val, partial);
-}
-
 // partials of b_i^2
 template <int BP>
 __global__ void __launch_bounds__(kBlock) k_sumsq(int n, int nrhs, const double* __restrict__ b,
@@ -216,18 +202,49 @@ __global__ void k_denom(int nrhs, const double* __restrict__ bn, double* __restr
     if (l < nrhs) denom[l] = bn[l] > 0.0 ? bn[l] : 1.0;
 }
 
-// b -= (sum w b) / (sum w)   (multigrid.cpp:240-250)
+// project_compatible sums (multigrid.cpp:240-250), in the reference's exact
+// order: `mean += w[i] * b[i]; total += w[i];` for i ascending, one thread per
+// right-hand side. A constant offset in b lies outside range(L), so any other
+// summation order leaves a permanent residual floor of a few ulps * sqrt(n)
+// that would show up in the per-cycle history; this keeps it bit-identical.
+// The loads are batched ahead of the dependent add chain.
+__global__ void k_project_sums(int n, int nrhs, const double* __restrict__ w, const double* __restrict__ b,
+                               double* __restrict__ mean_out) {
+    const int lane = threadIdx.x;
+    if (lane >= nrhs) return;
+    constexpr int U = 16;
+    double mean = 0.0, total = 0.0;
+    int i = 0;
+    for (; i + U <= n; i += U) {
+        double wv[U], bv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            wv[u] = w[i + u];
+            bv[u] = b[static_cast<int64_t>(i + u) * nrhs + lane];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            mean = __dadd_rn(mean, __dmul_rn(wv[u], bv[u]));
+            total = __dadd_rn(total, wv[u]);
+        }
+    }
+    for (; i < n; ++i) {
+        mean = __dadd_rn(mean, __dmul_rn(w[i], b[static_cast<int64_t>(i) * nrhs + lane]));
+        total = __dadd_rn(total, w[i]);
+    }
+    mean_out[lane] = __ddiv_rn(mean, total);
+}
+
+// b -= mean (per right-hand side)
 template <int BP>
-__global__ void __launch_bounds__(kBlock) k_project(int n, int nrhs, const double* __restrict__ num,
-                                                    const double* __restrict__ tot,
+__global__ void __launch_bounds__(kBlock) k_project(int n, int nrhs, const double* __restrict__ mean,
                                                     double* __restrict__ b) {
     const int64_t t = gtid();
     const int64_t row = t / BP;
     const int lane = static_cast<int>(t % BP);
     if (row >= n || lane >= nrhs) return;
-    const double mean = __ddiv_rn(num[lane], tot[0]);
     const int64_t o = row * nrhs + lane;
-    b[o] = __dsub_rn(b[o], mean);
+    b[o] = __dsub_rn(b[o], mean[lane]);
 }
 
 // Coarse solve: the projected weighted CG of oracle/ref_standin_direct.cpp,
@@ -557,20 +574,13 @@ Status project_compatible(decmg_gpu_ctx* c, int nrhs, double* d_b) {
     DG_TRY(check_nrhs(c, nrhs));
     const int bp = bp_of(nrhs);
     const Level& L = c->lv[0];
-    double* num = c->dsmall + 128;
-    double* tot = c->dsmall + 192;
+    double* mean = c->dsmall + 128;
+    DG_TRY(launch(c, kNorms, 8.0 * L.nv * (nrhs + 1), [&] {
+        k_project_sums<<<1, 32, 0, c->stream>>>(L.nv, nrhs, L.area, d_b, mean);
+    }));
     const unsigned g = grid_for(static_cast<int64_t>(L.nv) * bp, kBlock);
     DG_TRY(launch(c, kNorms, 16.0 * L.nv * nrhs, [&] {
-        DISPATCH_BP(bp, k_wsum<BP><<<g, kBlock, 0, c->stream>>>(L.nv, nrhs, L.area, d_b, c->red));
-    }));
-    DG_TRY(launch(c, kNorms, 0.0, [&] { k_reduce<<<nrhs, kBlock, 0, c->stream>>>(g, bp, c->red, num, 0, nullptr); }));
-    const unsigned g1 = grid_for(L.nv, kBlock);
-    DG_TRY(launch(c, kNorms, 8.0 * L.nv, [&] {
-        k_wsum<1><<<g1, kBlock, 0, c->stream>>>(L.nv, 1, L.area, nullptr, c->red);
-    }));
-    DG_TRY(launch(c, kNorms, 0.0, [&] { k_reduce<<<1, kBlock, 0, c->stream>>>(g1, 1, c->red, tot, 0, nullptr); }));
-    DG_TRY(launch(c, kNorms, 16.0 * L.nv * nrhs, [&] {
-        DISPATCH_BP(bp, k_project<BP><<<g, kBlock, 0, c->stream>>>(L.nv, nrhs, num, tot, d_b));
+        DISPATCH_BP(bp, k_project<BP><<<g, kBlock, 0, c->stream>>>(L.nv, nrhs, mean, d_b));
     }));
     return Status::Ok();
 }
