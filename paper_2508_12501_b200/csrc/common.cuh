@@ -68,6 +68,20 @@ struct Level {
     int* R_ci = nullptr;
     double* R_v = nullptr;
     int64_t nnzR = 0;
+    // Locality-ordered copies used by the hot kernels:
+    // row r of an *o array is row ord[r] of the reference-layout array, with
+    // its entries in the reference order, so every row sum is bit-identical;
+    // vectors keep the reference vertex numbering. ord == nullptr: identity.
+    int* ord = nullptr;      // [nv] Morton order of the vertex positions
+    int* Lo_rp = nullptr;
+    int* Lo_ci = nullptr;
+    double* Lo_v = nullptr;
+    int* Po_rp = nullptr;    // fine rows of P in this level's order
+    int* Po_ci = nullptr;
+    double* Po_v = nullptr;
+    int* Ro_rp = nullptr;    // coarse rows of R in the coarse level's order
+    int* Ro_ci = nullptr;
+    double* Ro_v = nullptr;
     int zero_diag_row = -1;  // first row with L_ii == 0 (-1: none)
     double wtot = 0.0;       // sum of dual areas, sequential (coarse solve)
     // work vectors [nv][max_nrhs]

@@ -55,14 +55,16 @@ template <int BP>
 __global__ void __launch_bounds__(kBlock) k_sweep(int n, int nrhs, const int* __restrict__ rp,
                                                   const int* __restrict__ ci,
                                                   const double* __restrict__ v,
+                                                  const int* __restrict__ rowid,
                                                   const double* __restrict__ x,
                                                   const double* __restrict__ b,
                                                   double* __restrict__ xo, double omega) {
     const int64_t t = gtid();
-    const int64_t row = t / BP;
+    const int64_t r = t / BP;
     const int lane = static_cast<int>(t % BP);
-    if (row >= n || lane >= nrhs) return;
-    const int k0 = rp[row], k1 = rp[row + 1];
+    if (r >= n || lane >= nrhs) return;
+    const int64_t row = rowid ? rowid[r] : r;
+    const int k0 = rp[r], k1 = rp[r + 1];
     double s = 0.0, d = 0.0, xr = 0.0;
     for (int k = k0; k < k1; ++k) {
         const int c = ci[k];
@@ -100,17 +102,19 @@ template <int BP, bool STORE>
 __global__ void __launch_bounds__(kBlock) k_residual(int n, int nrhs, const int* __restrict__ rp,
                                                      const int* __restrict__ ci,
                                                      const double* __restrict__ v,
+                                                     const int* __restrict__ rowid,
                                                      const double* __restrict__ x,
                                                      const double* __restrict__ b,
                                                      double* __restrict__ r,
                                                      double* __restrict__ partial) {
     const int64_t t = gtid();
-    const int64_t row = t / BP;
+    const int64_t q = t / BP;
     const int lane = static_cast<int>(t % BP);
-    const bool valid = row < n && lane < nrhs;
+    const bool valid = q < n && lane < nrhs;
     double rv = 0.0;
     if (valid) {
-        const int k0 = rp[row], k1 = rp[row + 1];
+        const int64_t row = rowid ? rowid[q] : q;
+        const int k0 = rp[q], k1 = rp[q + 1];
         double s = 0.0;
         for (int k = k0; k < k1; ++k)
             s = __dadd_rn(s, __dmul_rn(v[k], x[static_cast<int64_t>(ci[k]) * nrhs + lane]));
@@ -127,15 +131,17 @@ template <int BP>
 __global__ void __launch_bounds__(kBlock) k_spmv(int nrows, int nrhs, const int* __restrict__ rp,
                                                  const int* __restrict__ ci,
                                                  const double* __restrict__ v,
+                                                 const int* __restrict__ rowid,
                                                  const double* __restrict__ x,
                                                  double* __restrict__ y,
                                                  const int* __restrict__ zero_rows) {
     const int64_t t = gtid();
-    const int64_t row = t / BP;
+    const int64_t r = t / BP;
     const int lane = static_cast<int>(t % BP);
-    if (row >= nrows || lane >= nrhs) return;
+    if (r >= nrows || lane >= nrhs) return;
+    const int64_t row = rowid ? rowid[r] : r;
     double s = 0.0;
-    for (int k = rp[row]; k < rp[row + 1]; ++k)
+    for (int k = rp[r]; k < rp[r + 1]; ++k)
         s = __dadd_rn(s, __dmul_rn(v[k], x[static_cast<int64_t>(ci[k]) * nrhs + lane]));
     if (zero_rows && zero_rows[row]) s = 0.0;
     y[row * nrhs + lane] = s;
@@ -147,14 +153,16 @@ template <int BP>
 __global__ void __launch_bounds__(kBlock) k_prolong_add(int n, int nrhs, const int* __restrict__ rp,
                                                         const int* __restrict__ ci,
                                                         const double* __restrict__ v,
+                                                        const int* __restrict__ rowid,
                                                         const double* __restrict__ xc,
                                                         double* __restrict__ xf) {
     const int64_t t = gtid();
-    const int64_t row = t / BP;
+    const int64_t r = t / BP;
     const int lane = static_cast<int>(t % BP);
-    if (row >= n || lane >= nrhs) return;
+    if (r >= n || lane >= nrhs) return;
+    const int64_t row = rowid ? rowid[r] : r;
     double s = 0.0;
-    for (int k = rp[row]; k < rp[row + 1]; ++k)
+    for (int k = rp[r]; k < rp[r + 1]; ++k)
         s = __dadd_rn(s, __dmul_rn(v[k], xc[static_cast<int64_t>(ci[k]) * nrhs + lane]));
     const int64_t o = row * nrhs + lane;
     xf[o] = __dadd_rn(xf[o], s);
@@ -203,36 +211,103 @@ __global__ void k_denom(int nrhs, const double* __restrict__ bn, double* __restr
 }
 
 // project_compatible sums (multigrid.cpp:240-250), in the reference's exact
-// order: `mean += w[i] * b[i]; total += w[i];` for i ascending, one thread per
+// order: `mean += w[i] * b[i]; total += w[i];` for i ascending, one lane per
 // right-hand side. A constant offset in b lies outside range(L), so any other
 // summation order leaves a permanent residual floor of a few ulps * sqrt(n)
 // that would show up in the per-cycle history; this keeps it bit-identical.
-// The loads are batched ahead of the dependent add chain.
-__global__ void k_project_sums(int n, int nrhs, const double* __restrict__ w, const double* __restrict__ b,
-                               double* __restrict__ mean_out) {
-    const int lane = threadIdx.x;
-    if (lane >= nrhs) return;
-    constexpr int U = 16;
-    double mean = 0.0, total = 0.0;
-    int i = 0;
-    for (; i + U <= n; i += U) {
-        double wv[U], bv[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            wv[u] = w[i + u];
-            bv[u] = b[static_cast<int64_t>(i + u) * nrhs + lane];
+//
+// The sum is a dependent add chain, so the kernel is built to run at the
+// DADD latency: one producer thread streams [CH rows x nrhs] tiles of b and
+// the matching w tiles into a kStages-deep shared-memory ring with TMA bulk
+// copies (cp.async.bulk + mbarrier complete_tx), and warp 0 consumes them.
+constexpr int kProjStages = 4;
+constexpr int kProjRows = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(64) k_project_sums(int n, int nrhs, const double* __restrict__ w,
+                                                     const double* __restrict__ b,
+                                                     double* __restrict__ mean_out) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* bbuf = reinterpret_cast<double*>(smem_raw);                       // [S][CH*nrhs]
+    double* wbuf = bbuf + static_cast<size_t>(kProjStages) * kProjRows * nrhs;  // [S][CH]
+    __shared__ __align__(8) uint64_t full[kProjStages], empty[kProjStages];
+    const int nchunks = n / kProjRows;  // full tiles; the tail is read directly
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kProjStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
         }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            mean = __dadd_rn(mean, __dmul_rn(wv[u], bv[u]));
-            total = __dadd_rn(total, wv[u]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 32) {
+        // producer
+        const uint32_t bbytes = kProjRows * nrhs * sizeof(double), wbytes = kProjRows * sizeof(double);
+        for (int c = 0; c < nchunks; ++c) {
+            const int s = c % kProjStages;
+            if (c >= kProjStages) mbar_wait(&empty[s], ((c / kProjStages) - 1) & 1);
+            mbar_expect_tx(&full[s], bbytes + wbytes);
+            tma_bulk_g2s(bbuf + static_cast<size_t>(s) * kProjRows * nrhs,
+                         b + static_cast<int64_t>(c) * kProjRows * nrhs, bbytes, &full[s]);
+            tma_bulk_g2s(wbuf + s * kProjRows, w + static_cast<int64_t>(c) * kProjRows, wbytes, &full[s]);
+        }
+    } else if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        double mean = 0.0, total = 0.0;
+        for (int c = 0; c < nchunks; ++c) {
+            const int s = c % kProjStages;
+            mbar_wait(&full[s], (c / kProjStages) & 1);
+            const double* bt = bbuf + static_cast<size_t>(s) * kProjRows * nrhs;
+            const double* wt = wbuf + s * kProjRows;
+            if (lane < nrhs) {
+#pragma unroll 8
+                for (int i = 0; i < kProjRows; ++i) {
+                    const double wv = wt[i];
+                    mean = __dadd_rn(mean, __dmul_rn(wv, bt[i * nrhs + lane]));
+                    total = __dadd_rn(total, wv);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        if (lane < nrhs) {
+            for (int i = nchunks * kProjRows; i < n; ++i) {
+                const double wv = w[i];
+                mean = __dadd_rn(mean, __dmul_rn(wv, b[static_cast<int64_t>(i) * nrhs + lane]));
+                total = __dadd_rn(total, wv);
+            }
+            mean_out[lane] = __ddiv_rn(mean, total);
         }
     }
-    for (; i < n; ++i) {
-        mean = __dadd_rn(mean, __dmul_rn(w[i], b[static_cast<int64_t>(i) * nrhs + lane]));
-        total = __dadd_rn(total, w[i]);
-    }
-    mean_out[lane] = __ddiv_rn(mean, total);
 }
 
 // b -= mean (per right-hand side)
@@ -372,7 +447,7 @@ struct Driver {
                 const double* x = xcur(L);
                 DG_TRY(launch(c, k == 0 ? kFineSweep : kCoarseLevels, bytes, [&] {
                     DISPATCH_BP(bp, k_sweep<BP><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                        L.nv, nrhs, L.L_rp, L.L_ci, L.L_v, x, b, xo, plan.omega));
+                                        L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b, xo, plan.omega));
                 }));
             }
             L.cur ^= 1;
@@ -392,13 +467,13 @@ struct Driver {
         const double rbytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
         DG_TRY(launch(c, k == 0 ? kFineResidual : kCoarseLevels, rbytes, [&] {
             DISPATCH_BP(bp, (k_residual<BP, true><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                L.nv, nrhs, L.L_rp, L.L_ci, L.L_v, x, b, c->r, nullptr)));
+                                L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b, c->r, nullptr)));
         }));
         const double tbytes = 12.0 * L.nnzR + 4.0 * (C.nv + 1) + 8.0 * L.nv * R + 8.0 * C.nv * R;
         const int* zr = c->dirichlet ? C.bd : nullptr;
         DG_TRY(launch(c, k == 0 ? kRestrict : kCoarseLevels, tbytes, [&] {
             DISPATCH_BP(bp, k_spmv<BP><<<rows_grid(C.nv), kBlock, 0, c->stream>>>(
-                                C.nv, nrhs, L.R_rp, L.R_ci, L.R_v, c->r, C.b, zr));
+                                C.nv, nrhs, L.Ro_rp, L.Ro_ci, L.Ro_v, C.ord, c->r, C.b, zr));
         }));
         return Status::Ok();
     }
@@ -415,7 +490,7 @@ struct Driver {
         double* xf = xcur(L);
         DG_TRY(launch(c, k == 0 ? kProlong : kCoarseLevels, bytes, [&] {
             DISPATCH_BP(bp, k_prolong_add<BP><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                L.nv, nrhs, L.P_rp, L.P_ci, L.P_v, xc, xf));
+                                L.nv, nrhs, L.Po_rp, L.Po_ci, L.Po_v, L.ord, xc, xf));
         }));
         return Status::Ok();
     }
@@ -480,7 +555,7 @@ struct Driver {
         const double bytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 16.0 * L.nv * nrhs;
         DG_TRY(launch(c, kFineResidual, bytes, [&] {
             DISPATCH_BP(bp, (k_residual<BP, false><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                L.nv, nrhs, L.L_rp, L.L_ci, L.L_v, x, b0, nullptr, c->red)));
+                                L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b0, nullptr, c->red)));
         }));
         DG_TRY(launch(c, kNorms, 0.0, [&] {
             k_reduce<<<nrhs, kBlock, 0, c->stream>>>(partial_blocks(L.nv), bp, c->red, hist, 2, denom);
@@ -575,8 +650,13 @@ Status project_compatible(decmg_gpu_ctx* c, int nrhs, double* d_b) {
     const int bp = bp_of(nrhs);
     const Level& L = c->lv[0];
     double* mean = c->dsmall + 128;
+    // TMA bulk copies need 16-byte aligned sources (cudaMalloc'd buffers are)
+    if ((reinterpret_cast<uintptr_t>(d_b) & 15) != 0)
+        return Status::Err(DECMG_INVALID_ARGUMENT, "project_compatible: rhs must be 16-byte aligned");
+    const size_t smem = static_cast<size_t>(kProjStages) * kProjRows * (nrhs + 1) * sizeof(double);
+    DG_CUDA(cudaFuncSetAttribute(k_project_sums, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     DG_TRY(launch(c, kNorms, 8.0 * L.nv * (nrhs + 1), [&] {
-        k_project_sums<<<1, 32, 0, c->stream>>>(L.nv, nrhs, L.area, d_b, mean);
+        k_project_sums<<<1, 64, smem, c->stream>>>(L.nv, nrhs, L.area, d_b, mean);
     }));
     const unsigned g = grid_for(static_cast<int64_t>(L.nv) * bp, kBlock);
     DG_TRY(launch(c, kNorms, 16.0 * L.nv * nrhs, [&] {
@@ -669,7 +749,7 @@ Status apply_op(decmg_gpu_ctx* c, int level, char op, const double* d_x, double*
         return Status::Err(DECMG_INVALID_ARGUMENT, "apply: unknown operator for this level");
     }
     DG_TRY(launch(c, kNorms, 0.0, [&] {
-        k_spmv<1><<<grid_for(rows, kBlock), kBlock, 0, c->stream>>>(rows, 1, rp, ci, v, d_x, d_y, nullptr);
+        k_spmv<1><<<grid_for(rows, kBlock), kBlock, 0, c->stream>>>(rows, 1, rp, ci, v, nullptr, d_x, d_y, nullptr);
     }));
     return Status::Ok();
 }

@@ -12,9 +12,12 @@
 // Integer structure (edge numbering, triangle edge triples, CSR) is built with
 // counting sorts: counts (atomics, order-free) -> exclusive scan -> fill ->
 // per-segment insertion sort, so the result never depends on thread timing.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
+
+#include <cstring>
 
 namespace decmg_gpu {
 namespace {
@@ -421,6 +424,86 @@ __global__ void k_R_fill(int nvc, const int* __restrict__ ve_ptr, const int* __r
     }
 }
 
+// ------------------------------------------------------------ row order ----
+// Processing order for the hot kernels: vertices sorted by the Morton code of
+// their position (21 bits per axis inside the mesh bounding box), ties by id.
+// Spatial neighbours then sit in nearby rows, so the gathers of x[col] of the
+// rows in flight hit L2 instead of HBM. The order only changes which thread
+// computes which row, never the arithmetic of a row.
+__device__ __forceinline__ unsigned long long okey(double d) {
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(d));
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ULL);
+}
+
+__global__ void k_bbox(int n, const double* __restrict__ pos, unsigned long long* mm) {
+    __shared__ unsigned long long lo[3][kBlock], hi[3][kBlock];
+    const int64_t i = gtid();
+    for (int c = 0; c < 3; ++c) {
+        const unsigned long long k = i < n ? okey(pos[3 * i + c]) : 0;
+        lo[c][threadIdx.x] = i < n ? k : ~0ULL;
+        hi[c][threadIdx.x] = i < n ? k : 0ULL;
+    }
+    __syncthreads();
+    for (int s = kBlock / 2; s >= 1; s >>= 1) {
+        if (threadIdx.x < s)
+            for (int c = 0; c < 3; ++c) {
+                lo[c][threadIdx.x] = min(lo[c][threadIdx.x], lo[c][threadIdx.x + s]);
+                hi[c][threadIdx.x] = max(hi[c][threadIdx.x], hi[c][threadIdx.x + s]);
+            }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int c = 0; c < 3; ++c) {
+            atomicMin(&mm[c], lo[c][0]);
+            atomicMax(&mm[3 + c], hi[c][0]);
+        }
+}
+
+__device__ __forceinline__ unsigned long long spread3(unsigned long long x) {
+    x &= 0x1fffffULL;
+    x = (x | x << 32) & 0x1f00000000ffffULL;
+    x = (x | x << 16) & 0x1f0000ff0000ffULL;
+    x = (x | x << 8) & 0x100f00f00f00f00fULL;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ULL;
+    x = (x | x << 2) & 0x1249249249249249ULL;
+    return x;
+}
+
+__global__ void k_morton(int n, const double* __restrict__ pos, double lx, double ly, double lz, double sx,
+                         double sy, double sz, unsigned long long* __restrict__ key, int* __restrict__ id) {
+    const int64_t i = gtid();
+    if (i >= n) return;
+    const double lo[3] = {lx, ly, lz}, sc[3] = {sx, sy, sz};
+    unsigned long long q[3];
+    for (int c = 0; c < 3; ++c) {
+        double f = (pos[3 * i + c] - lo[c]) * sc[c];
+        f = f < 0.0 ? 0.0 : (f > 2097151.0 ? 2097151.0 : f);
+        q[c] = static_cast<unsigned long long>(f);
+    }
+    key[i] = spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2);
+    id[i] = static_cast<int>(i);
+}
+
+__global__ void k_perm_count(int n, const int* __restrict__ ord, const int* __restrict__ rp, int* cnt) {
+    const int64_t r = gtid();
+    if (r >= n) return;
+    const int o = ord[r];
+    cnt[r] = rp[o + 1] - rp[o];
+}
+
+__global__ void k_perm_fill(int n, const int* __restrict__ ord, const int* __restrict__ rp,
+                            const int* __restrict__ ci, const double* __restrict__ v,
+                            const int* __restrict__ orp, int* __restrict__ oci, double* __restrict__ ov) {
+    const int64_t r = gtid();
+    if (r >= n) return;
+    const int o = ord[r];
+    const int src = rp[o], len = rp[o + 1] - src, dst = orp[r];
+    for (int k = 0; k < len; ++k) {
+        oci[dst + k] = ci[src + k];
+        ov[dst + k] = v[src + k];
+    }
+}
+
 // ------------------------------------------------------------ helpers ------
 struct TmpPool {
     cudaStream_t s;
@@ -589,6 +672,89 @@ Status assemble(decmg_gpu_ctx* c, Level& m, bool dirichlet) {
     return Status::Ok();
 }
 
+Status morton_order(decmg_gpu_ctx* c, Level& m) {
+    TmpPool tp(c->stream);
+    unsigned long long* mm;
+    DG_TRY(tp.get(&mm, 6));
+    const unsigned long long init[6] = {~0ULL, ~0ULL, ~0ULL, 0ULL, 0ULL, 0ULL};
+    DG_CUDA(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, c->stream));
+    LAUNCH(4, m.nv, k_bbox, m.nv, m.pos, mm);
+    unsigned long long h[6];
+    DG_CUDA(cudaMemcpyAsync(h, mm, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    DG_CUDA(cudaStreamSynchronize(c->stream));
+    double lo[3], sc[3];
+    for (int k = 0; k < 3; ++k) {
+        auto dec = [](unsigned long long u) {
+            u = (u >> 63) ? (u & 0x7fffffffffffffffULL) : ~u;
+            double d;
+            std::memcpy(&d, &u, sizeof d);
+            return d;
+        };
+        lo[k] = dec(h[k]);
+        const double ext = dec(h[3 + k]) - lo[k];
+        sc[k] = ext > 0.0 ? 2097151.0 / ext : 0.0;
+    }
+    unsigned long long *kin, *kout;
+    int *iin;
+    DG_TRY(tp.get(&kin, m.nv));
+    DG_TRY(tp.get(&kout, m.nv));
+    DG_TRY(tp.get(&iin, m.nv));
+    DG_TRY(dalloc(c, &m.ord, m.nv));
+    LAUNCH(4, m.nv, k_morton, m.nv, m.pos, lo[0], lo[1], lo[2], sc[0], sc[1], sc[2], kin, iin);
+    size_t bytes = 0;
+    DG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, iin, m.ord, m.nv, 0, 64, c->stream));
+    void* tmp;
+    DG_TRY(tp.get(reinterpret_cast<char**>(&tmp), bytes));
+    DG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, iin, m.ord, m.nv, 0, 64, c->stream));
+    return Status::Ok();
+}
+
+Status permute_rows(decmg_gpu_ctx* c, int nrows, const int* ord, const int* rp, const int* ci, const double* v,
+                    int64_t nnz, int** orp, int** oci, double** ov) {
+    TmpPool tp(c->stream);
+    int* cnt;
+    DG_TRY(tp.get(&cnt, nrows + 1));
+    DG_CUDA(cudaMemsetAsync(cnt, 0, (nrows + 1) * sizeof(int), c->stream));
+    DG_TRY(dalloc(c, orp, nrows + 1));
+    DG_TRY(dalloc(c, oci, nnz));
+    DG_TRY(dalloc(c, ov, nnz));
+    LAUNCH(4, nrows, k_perm_count, nrows, ord, rp, cnt);
+    DG_TRY(exclusive_scan(c, cnt, *orp, nrows));
+    LAUNCH(4, nrows, k_perm_fill, nrows, ord, rp, ci, v, *orp, *oci, *ov);
+    return Status::Ok();
+}
+
+// Row orders for every level except the coarsest (its CG runs sequentially
+// in the reference order), then the reordered L, P and R.
+Status build_orders(decmg_gpu_ctx* c) {
+    const int L = static_cast<int>(c->lv.size());
+    for (int k = 0; k + 1 < L; ++k)
+        if (c->lv[k].pos) DG_TRY(morton_order(c, c->lv[k]));
+    for (int k = 0; k < L; ++k) {
+        Level& m = c->lv[k];
+        if (m.ord) {
+            DG_TRY(permute_rows(c, m.nv, m.ord, m.L_rp, m.L_ci, m.L_v, m.nnzL, &m.Lo_rp, &m.Lo_ci, &m.Lo_v));
+        } else {
+            m.Lo_rp = m.L_rp; m.Lo_ci = m.L_ci; m.Lo_v = m.L_v;
+        }
+        if (k + 1 < L) {
+            if (m.ord) {
+                DG_TRY(permute_rows(c, m.nv, m.ord, m.P_rp, m.P_ci, m.P_v, m.nnzP, &m.Po_rp, &m.Po_ci, &m.Po_v));
+            } else {
+                m.Po_rp = m.P_rp; m.Po_ci = m.P_ci; m.Po_v = m.P_v;
+            }
+            const Level& cm = c->lv[k + 1];
+            if (cm.ord) {
+                DG_TRY(permute_rows(c, cm.nv, cm.ord, m.R_rp, m.R_ci, m.R_v, m.nnzR, &m.Ro_rp, &m.Ro_ci, &m.Ro_v));
+            } else {
+                m.Ro_rp = m.R_rp; m.Ro_ci = m.R_ci; m.Ro_v = m.R_v;
+            }
+        }
+    }
+    DG_CUDA(cudaStreamSynchronize(c->stream));
+    return Status::Ok();
+}
+
 }  // namespace
 
 Status exclusive_scan(decmg_gpu_ctx* c, const int* in, int* out, int n) {
@@ -664,6 +830,7 @@ Status build_from_base(decmg_gpu_ctx* c, const double* hpos, int nv, const int* 
         for (double x : a) wt += x;
         cl.wtot = wt;
     }
+    DG_TRY(build_orders(c));
     DG_TRY(alloc_work(c));
     DG_CUDA(cudaStreamSynchronize(c->stream));
     return Status::Ok();
@@ -725,6 +892,7 @@ Status build_from_levels(decmg_gpu_ctx* c, const decmg_gpu_level_desc* d, int L,
             DG_CUDA(cudaMemcpy(m.R_v, s.R_values, sizeof(double) * m.nnzR, cudaMemcpyHostToDevice));
         }
     }
+    DG_TRY(build_orders(c));
     DG_TRY(alloc_work(c));
     return Status::Ok();
 }
