@@ -48,11 +48,58 @@ __device__ __forceinline__ void block_partial(double v, double* partial) {
     if (threadIdx.x < BP) partial[static_cast<int64_t>(blockIdx.x) * BP + threadIdx.x] = sh[threadIdx.x];
 }
 
+// Row dot product in the reference order (s = 0.0; s += v_k * x[c_k]) with the
+// loads batched for memory-level parallelism: all column indices and values of
+// the row first, then all gathers, then the ordered sum. Rows of up to kMaxRow
+// entries (every vertex of valence <= 7) take the unrolled path; longer rows
+// fall back to the plain loop. DIAG also returns the diagonal entry and x_ii.
+constexpr int kMaxRow = 8;
+template <bool DIAG>
+__device__ __forceinline__ double row_dot(int k0, int len, const int* __restrict__ ci,
+                                          const double* __restrict__ v, const double* __restrict__ x,
+                                          int nrhs, int lane, int64_t row, double* d, double* xr) {
+    double s = 0.0;
+    if (len <= kMaxRow) {
+        int cc[kMaxRow];
+        double vv[kMaxRow], xv[kMaxRow];
+#pragma unroll
+        for (int j = 0; j < kMaxRow; ++j)
+            if (j < len) {
+                cc[j] = __ldg(ci + k0 + j);
+                vv[j] = __ldg(v + k0 + j);
+            }
+#pragma unroll
+        for (int j = 0; j < kMaxRow; ++j)
+            if (j < len) xv[j] = x[static_cast<int64_t>(cc[j]) * nrhs + lane];
+#pragma unroll
+        for (int j = 0; j < kMaxRow; ++j)
+            if (j < len) {
+                s = __dadd_rn(s, __dmul_rn(vv[j], xv[j]));
+                if (DIAG && cc[j] == row) {
+                    *d = vv[j];
+                    *xr = xv[j];
+                }
+            }
+    } else {
+        for (int k = k0; k < k0 + len; ++k) {
+            const int c = ci[k];
+            const double a = v[k];
+            const double xx = x[static_cast<int64_t>(c) * nrhs + lane];
+            s = __dadd_rn(s, __dmul_rn(a, xx));
+            if (DIAG && c == row) {
+                *d = a;
+                *xr = xx;
+            }
+        }
+    }
+    return s;
+}
+
 // jacobi_sweep: s = A x (CSR order), x' = x + (omega (b - s)) / a_ii.
 // x is read entirely before any write (ping-pong buffers), as in the
 // reference, where A.apply fills scratch before the update loop.
 template <int BP>
-__global__ void __launch_bounds__(kBlock) k_sweep(int n, int nrhs, const int* __restrict__ rp,
+__global__ void __launch_bounds__(kBlock, 4) k_sweep(int n, int nrhs, const int* __restrict__ rp,
                                                   const int* __restrict__ ci,
                                                   const double* __restrict__ v,
                                                   const int* __restrict__ rowid,
@@ -64,20 +111,12 @@ __global__ void __launch_bounds__(kBlock) k_sweep(int n, int nrhs, const int* __
     const int lane = static_cast<int>(t % BP);
     if (r >= n || lane >= nrhs) return;
     const int64_t row = rowid ? rowid[r] : r;
-    const int k0 = rp[r], k1 = rp[r + 1];
-    double s = 0.0, d = 0.0, xr = 0.0;
-    for (int k = k0; k < k1; ++k) {
-        const int c = ci[k];
-        const double a = v[k];
-        const double xv = x[static_cast<int64_t>(c) * nrhs + lane];
-        s = __dadd_rn(s, __dmul_rn(a, xv));
-        if (c == row) {
-            d = a;
-            xr = xv;
-        }
-    }
+    const int k0 = rp[r], len = rp[r + 1] - k0;
     const int64_t o = row * nrhs + lane;
-    xo[o] = __dadd_rn(xr, __ddiv_rn(__dmul_rn(omega, __dsub_rn(b[o], s)), d));
+    const double bo = b[o];
+    double d = 0.0, xr = 0.0;
+    const double s = row_dot<true>(k0, len, ci, v, x, nrhs, lane, row, &d, &xr);
+    xo[o] = __dadd_rn(xr, __ddiv_rn(__dmul_rn(omega, __dsub_rn(bo, s)), d));
 }
 
 // First sweep after kernels::fill(0.0, x) (multigrid.cpp:268): A * 0 is
@@ -99,7 +138,7 @@ __global__ void __launch_bounds__(kBlock) k_sweep_zero(int n, int nrhs,
 // r = b - A x (multigrid.cpp:263-265 / 317-318); optionally stores r and/or
 // emits per-CTA partial sums of r^2 for the residual norm.
 template <int BP, bool STORE>
-__global__ void __launch_bounds__(kBlock) k_residual(int n, int nrhs, const int* __restrict__ rp,
+__global__ void __launch_bounds__(kBlock, 4) k_residual(int n, int nrhs, const int* __restrict__ rp,
                                                      const int* __restrict__ ci,
                                                      const double* __restrict__ v,
                                                      const int* __restrict__ rowid,
@@ -114,12 +153,11 @@ __global__ void __launch_bounds__(kBlock) k_residual(int n, int nrhs, const int*
     double rv = 0.0;
     if (valid) {
         const int64_t row = rowid ? rowid[q] : q;
-        const int k0 = rp[q], k1 = rp[q + 1];
-        double s = 0.0;
-        for (int k = k0; k < k1; ++k)
-            s = __dadd_rn(s, __dmul_rn(v[k], x[static_cast<int64_t>(ci[k]) * nrhs + lane]));
+        const int k0 = rp[q], len = rp[q + 1] - k0;
         const int64_t o = row * nrhs + lane;
-        rv = __dsub_rn(b[o], s);
+        const double bo = b[o];
+        const double s = row_dot<false>(k0, len, ci, v, x, nrhs, lane, row, nullptr, nullptr);
+        rv = __dsub_rn(bo, s);
         if (STORE) r[o] = rv;
     }
     if (partial) block_partial<BP>(valid ? __dmul_rn(rv, rv) : 0.0, partial);
@@ -140,9 +178,8 @@ __global__ void __launch_bounds__(kBlock) k_spmv(int nrows, int nrhs, const int*
     const int lane = static_cast<int>(t % BP);
     if (r >= nrows || lane >= nrhs) return;
     const int64_t row = rowid ? rowid[r] : r;
-    double s = 0.0;
-    for (int k = rp[r]; k < rp[r + 1]; ++k)
-        s = __dadd_rn(s, __dmul_rn(v[k], x[static_cast<int64_t>(ci[k]) * nrhs + lane]));
+    const int k0 = rp[r];
+    double s = row_dot<false>(k0, rp[r + 1] - k0, ci, v, x, nrhs, lane, row, nullptr, nullptr);
     if (zero_rows && zero_rows[row]) s = 0.0;
     y[row * nrhs + lane] = s;
 }
@@ -161,11 +198,11 @@ __global__ void __launch_bounds__(kBlock) k_prolong_add(int n, int nrhs, const i
     const int lane = static_cast<int>(t % BP);
     if (r >= n || lane >= nrhs) return;
     const int64_t row = rowid ? rowid[r] : r;
-    double s = 0.0;
-    for (int k = rp[r]; k < rp[r + 1]; ++k)
-        s = __dadd_rn(s, __dmul_rn(v[k], xc[static_cast<int64_t>(ci[k]) * nrhs + lane]));
     const int64_t o = row * nrhs + lane;
-    xf[o] = __dadd_rn(xf[o], s);
+    const double xo = xf[o];
+    const int k0 = rp[r];
+    const double s = row_dot<false>(k0, rp[r + 1] - k0, ci, v, xc, nrhs, lane, row, nullptr, nullptr);
+    xf[o] = __dadd_rn(xo, s);
 }
 
 // partials of b_i^2
@@ -180,29 +217,28 @@ __global__ void __launch_bounds__(kBlock) k_sumsq(int n, int nrhs, const double*
     block_partial<BP>(__dmul_rn(val, val), partial);
 }
 
-// Second stage: one CTA per lane sums its partials in a fixed order.
+// Partials are folded by repeated fixed-shape block reductions (each CTA folds
+// 256/BP consecutive partial rows), then finalized:
 // mode 0: out[lane] = total
 // mode 1: out[lane] = sqrt(total)                      (norm)
 // mode 2: out[lane] = sqrt(total) / denom[lane]         (relative residual)
-__global__ void k_reduce(int nblocks, int BP, const double* __restrict__ partial,
-                         double* __restrict__ out, int mode, const double* __restrict__ denom) {
-    __shared__ double sh[kBlock];
-    const int lane = blockIdx.x;
-    double acc = 0.0;
-    for (int blk = threadIdx.x; blk < nblocks; blk += kBlock)
-        acc = __dadd_rn(acc, partial[static_cast<int64_t>(blk) * BP + lane]);
-    sh[threadIdx.x] = acc;
-    __syncthreads();
-    for (int s = kBlock / 2; s >= 1; s >>= 1) {
-        if (threadIdx.x < s) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + s]);
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        const double tot = sh[0];
-        if (mode == 0) out[lane] = tot;
-        else if (mode == 1) out[lane] = __dsqrt_rn(tot);
-        else out[lane] = __ddiv_rn(__dsqrt_rn(tot), denom[lane]);
-    }
+template <int BP>
+__global__ void __launch_bounds__(kBlock) k_fold(int64_t nrows, const double* __restrict__ in,
+                                                 double* __restrict__ out) {
+    const int64_t t = gtid();
+    const int64_t row = t / BP;
+    const int lane = static_cast<int>(t % BP);
+    block_partial<BP>(row < nrows ? in[row * BP + lane] : 0.0, out);
+}
+
+__global__ void k_finalize(int nrhs, const double* __restrict__ tot, double* __restrict__ out, int mode,
+                           const double* __restrict__ denom) {
+    const int lane = threadIdx.x;
+    if (lane >= nrhs) return;
+    const double t = tot[lane];
+    if (mode == 0) out[lane] = t;
+    else if (mode == 1) out[lane] = __dsqrt_rn(t);
+    else out[lane] = __ddiv_rn(__dsqrt_rn(t), denom[lane]);
 }
 
 __global__ void k_denom(int nrhs, const double* __restrict__ bn, double* __restrict__ denom) {
@@ -535,16 +571,30 @@ struct Driver {
 
     int partial_blocks(int n) const { return static_cast<int>(rows_grid(n)); }
 
+    // Fold nrows partial rows ([nrows][bp] in c->red) down to one row.
+    Status reduce_partials(int64_t nrows, double* out, int mode, const double* denom) {
+        double* in = c->red;
+        double* nxt = c->red + c->red_cap / 2;
+        while (nrows > 1) {
+            const int64_t threads = nrows * bp;
+            const unsigned g = grid_for(threads, kBlock);
+            DG_TRY(launch(c, kNorms, 8.0 * threads, [&] {
+                DISPATCH_BP(bp, k_fold<BP><<<g, kBlock, 0, c->stream>>>(nrows, in, nxt));
+            }));
+            nrows = g;
+            std::swap(in, nxt);
+        }
+        DG_TRY(launch(c, kNorms, 0.0, [&] { k_finalize<<<1, 32, 0, c->stream>>>(nrhs, in, out, mode, denom); }));
+        return Status::Ok();
+    }
+
     // out[lane] = ||b||_2 over level-0 rows of vector v (mode 1) or sum (0)
     Status sumsq(const double* v, double* out, int mode) {
         const int n = c->lv[0].nv;
         DG_TRY(launch(c, kNorms, 8.0 * n * nrhs, [&] {
             DISPATCH_BP(bp, k_sumsq<BP><<<rows_grid(n), kBlock, 0, c->stream>>>(n, nrhs, v, c->red));
         }));
-        DG_TRY(launch(c, kNorms, 0.0, [&] {
-            k_reduce<<<nrhs, kBlock, 0, c->stream>>>(partial_blocks(n), bp, c->red, out, mode, nullptr);
-        }));
-        return Status::Ok();
+        return reduce_partials(partial_blocks(n), out, mode, nullptr);
     }
 
     // hist[lane] = ||b - A x||_2 / denom[lane] on level 0 (multigrid.cpp:317-319)
@@ -557,10 +607,7 @@ struct Driver {
             DISPATCH_BP(bp, (k_residual<BP, false><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
                                 L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b0, nullptr, c->red)));
         }));
-        DG_TRY(launch(c, kNorms, 0.0, [&] {
-            k_reduce<<<nrhs, kBlock, 0, c->stream>>>(partial_blocks(L.nv), bp, c->red, hist, 2, denom);
-        }));
-        return Status::Ok();
+        return reduce_partials(partial_blocks(L.nv), hist, 2, denom);
     }
 
     // denom[lane] = ||b|| > 0 ? ||b|| : 1   (multigrid.cpp:307-308)

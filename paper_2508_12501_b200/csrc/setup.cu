@@ -914,7 +914,7 @@ Status alloc_work(decmg_gpu_ctx* c) {
     DG_TRY(dalloc(c, &c->io_x, n0));
     int bp = 1;
     while (bp < B) bp *= 2;
-    c->red_cap = (static_cast<size_t>(c->lv[0].nv) * bp / 256 + 2) * bp + 64;
+    c->red_cap = 2 * ((static_cast<size_t>(c->lv[0].nv) * bp / 256 + 2) * bp + 64);
     DG_TRY(dalloc(c, &c->red, c->red_cap));
     DG_TRY(dalloc(c, &c->dsmall, 1024));
     DG_CUDA(cudaMallocHost(&c->hsmall, 1024 * sizeof(double)));
