@@ -33,35 +33,70 @@ __device__ __forceinline__ int64_t gtid() {
     return static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
 }
 
-// Fixed-shape block reduction of one value per thread into one partial per
-// lane: rows of the CTA are folded pairwise in a fixed order.
-template <int BP>
-__device__ __forceinline__ void block_partial(double v, double* partial) {
-    __shared__ double sh[kBlock];
-    sh[threadIdx.x] = v;
-    __syncthreads();
+// Thread mapping. A row is owned by TPR = BP / RPT consecutive threads and
+// each thread owns RPT consecutive right-hand sides (lanes sub*RPT ..
+// sub*RPT + RPT - 1), loaded with 16-byte vector accesses. RPT > 1 only when
+// nrhs == BP (full, 16-byte aligned rows). Per-lane arithmetic is unchanged,
+// so the mapping never affects the bits of a result.
+template <int RPT>
+__device__ __forceinline__ void ldv(const double* __restrict__ p, double (&o)[RPT]) {
+    if constexpr (RPT == 1) {
+        o[0] = *p;
+    } else {
 #pragma unroll
-    for (int s = kBlock / 2; s >= BP; s >>= 1) {
-        if (threadIdx.x < s) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + s]);
-        __syncthreads();
+        for (int j = 0; j < RPT / 2; ++j) {
+            const double2 t = *reinterpret_cast<const double2*>(p + 2 * j);
+            o[2 * j] = t.x;
+            o[2 * j + 1] = t.y;
+        }
     }
-    if (threadIdx.x < BP) partial[static_cast<int64_t>(blockIdx.x) * BP + threadIdx.x] = sh[threadIdx.x];
+}
+template <int RPT>
+__device__ __forceinline__ void stv(double* __restrict__ p, const double (&o)[RPT]) {
+    if constexpr (RPT == 1) {
+        *p = o[0];
+    } else {
+#pragma unroll
+        for (int j = 0; j < RPT / 2; ++j)
+            *reinterpret_cast<double2*>(p + 2 * j) = make_double2(o[2 * j], o[2 * j + 1]);
+    }
 }
 
-// Row dot product in the reference order (s = 0.0; s += v_k * x[c_k]) with the
-// loads batched for memory-level parallelism: all column indices and values of
-// the row first, then all gathers, then the ordered sum. Rows of up to kMaxRow
-// entries (every vertex of valence <= 7) take the unrolled path; longer rows
-// fall back to the plain loop. DIAG also returns the diagonal entry and x_ii.
+// Fixed-shape block reduction into one partial per lane: the CTA's rows are
+// folded pairwise in a fixed order (deterministic run to run).
+template <int BP, int RPT>
+__device__ __forceinline__ void block_partial(const double (&v)[RPT], double* partial) {
+    constexpr int TPR = BP / RPT, ROWS = kBlock / TPR;
+    __shared__ double sh[kBlock * RPT];  // [ROWS][BP]
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) sh[threadIdx.x * RPT + j] = v[j];
+    __syncthreads();
+#pragma unroll
+    for (int s = ROWS / 2; s >= 1; s >>= 1) {
+        for (int idx = threadIdx.x; idx < s * BP; idx += kBlock) sh[idx] = __dadd_rn(sh[idx], sh[idx + s * BP]);
+        __syncthreads();
+    }
+    for (int idx = threadIdx.x; idx < BP; idx += kBlock)
+        partial[static_cast<int64_t>(blockIdx.x) * BP + idx] = sh[idx];
+}
+
+// Row dot product in the reference order (s = 0.0; s += v_k * x[c_k], per
+// lane) with the loads batched for memory-level parallelism: all column
+// indices and values of the row, then all gathers, then the ordered sums.
+// Rows of up to kMaxRow entries (valence <= 7) take the unrolled path; longer
+// rows use the plain loop. DIAG also returns a_ii and x_ii.
 constexpr int kMaxRow = 8;
-template <bool DIAG>
-__device__ __forceinline__ double row_dot(int k0, int len, const int* __restrict__ ci,
-                                          const double* __restrict__ v, const double* __restrict__ x,
-                                          int nrhs, int lane, int64_t row, double* d, double* xr) {
-    double s = 0.0;
+template <int RPT, bool DIAG>
+__device__ __forceinline__ void row_dot(int k0, int len, const int* __restrict__ ci,
+                                        const double* __restrict__ v, const double* __restrict__ x, int nrhs,
+                                        int lane0, int64_t row, double (&s)[RPT], double* d,
+                                        double (&xr)[RPT]) {
+#pragma unroll
+    for (int l = 0; l < RPT; ++l) s[l] = 0.0;
     if (len <= kMaxRow) {
         int cc[kMaxRow];
-        double vv[kMaxRow], xv[kMaxRow];
+        double vv[kMaxRow];
+        double xv[kMaxRow][RPT];
 #pragma unroll
         for (int j = 0; j < kMaxRow; ++j)
             if (j < len) {
@@ -70,151 +105,172 @@ __device__ __forceinline__ double row_dot(int k0, int len, const int* __restrict
             }
 #pragma unroll
         for (int j = 0; j < kMaxRow; ++j)
-            if (j < len) xv[j] = x[static_cast<int64_t>(cc[j]) * nrhs + lane];
+            if (j < len) ldv<RPT>(x + static_cast<int64_t>(cc[j]) * nrhs + lane0, xv[j]);
 #pragma unroll
         for (int j = 0; j < kMaxRow; ++j)
             if (j < len) {
-                s = __dadd_rn(s, __dmul_rn(vv[j], xv[j]));
+#pragma unroll
+                for (int l = 0; l < RPT; ++l) s[l] = __dadd_rn(s[l], __dmul_rn(vv[j], xv[j][l]));
                 if (DIAG && cc[j] == row) {
                     *d = vv[j];
-                    *xr = xv[j];
+#pragma unroll
+                    for (int l = 0; l < RPT; ++l) xr[l] = xv[j][l];
                 }
             }
     } else {
         for (int k = k0; k < k0 + len; ++k) {
             const int c = ci[k];
             const double a = v[k];
-            const double xx = x[static_cast<int64_t>(c) * nrhs + lane];
-            s = __dadd_rn(s, __dmul_rn(a, xx));
+            double xx[RPT];
+            ldv<RPT>(x + static_cast<int64_t>(c) * nrhs + lane0, xx);
+#pragma unroll
+            for (int l = 0; l < RPT; ++l) s[l] = __dadd_rn(s[l], __dmul_rn(a, xx[l]));
             if (DIAG && c == row) {
                 *d = a;
-                *xr = xx;
+#pragma unroll
+                for (int l = 0; l < RPT; ++l) xr[l] = xx[l];
             }
         }
     }
-    return s;
 }
 
-// jacobi_sweep: s = A x (CSR order), x' = x + (omega (b - s)) / a_ii.
-// x is read entirely before any write (ping-pong buffers), as in the
-// reference, where A.apply fills scratch before the update loop.
-template <int BP>
-__global__ void __launch_bounds__(kBlock, 4) k_sweep(int n, int nrhs, const int* __restrict__ rp,
-                                                  const int* __restrict__ ci,
-                                                  const double* __restrict__ v,
-                                                  const int* __restrict__ rowid,
-                                                  const double* __restrict__ x,
-                                                  const double* __restrict__ b,
-                                                  double* __restrict__ xo, double omega) {
-    const int64_t t = gtid();
-    const int64_t r = t / BP;
-    const int lane = static_cast<int>(t % BP);
-    if (r >= n || lane >= nrhs) return;
+#define ROW_SETUP()                                        \
+    constexpr int TPR = BP / RPT;                          \
+    const int64_t t = gtid();                              \
+    const int64_t r = t / TPR;                             \
+    const int lane0 = static_cast<int>(t % TPR) * RPT;
+
+// jacobi_sweep (multigrid.cpp:36-56): s = A x (CSR order),
+// x' = x + (omega (b - s)) / a_ii. x is read entirely before any write
+// (ping-pong buffers), as in the reference, where A.apply fills scratch first.
+template <int BP, int RPT>
+__global__ void __launch_bounds__(kBlock, 2) k_sweep(int n, int nrhs, const int* __restrict__ rp,
+                                                     const int* __restrict__ ci, const double* __restrict__ v,
+                                                     const int* __restrict__ rowid, const double* __restrict__ x,
+                                                     const double* __restrict__ b, double* __restrict__ xo,
+                                                     double omega) {
+    ROW_SETUP();
+    if (r >= n || lane0 >= nrhs) return;
     const int64_t row = rowid ? rowid[r] : r;
-    const int k0 = rp[r], len = rp[r + 1] - k0;
-    const int64_t o = row * nrhs + lane;
-    const double bo = b[o];
-    double d = 0.0, xr = 0.0;
-    const double s = row_dot<true>(k0, len, ci, v, x, nrhs, lane, row, &d, &xr);
-    xo[o] = __dadd_rn(xr, __ddiv_rn(__dmul_rn(omega, __dsub_rn(bo, s)), d));
+    const int64_t o = row * nrhs + lane0;
+    double bo[RPT], s[RPT], xr[RPT], out[RPT];
+    ldv<RPT>(b + o, bo);
+    const int k0 = rp[r];
+    double d = 0.0;
+    row_dot<RPT, true>(k0, rp[r + 1] - k0, ci, v, x, nrhs, lane0, row, s, &d, xr);
+#pragma unroll
+    for (int l = 0; l < RPT; ++l) out[l] = __dadd_rn(xr[l], __ddiv_rn(__dmul_rn(omega, __dsub_rn(bo[l], s[l])), d));
+    stv<RPT>(xo + o, out);
 }
 
 // First sweep after kernels::fill(0.0, x) (multigrid.cpp:268): A * 0 is
 // exactly +0.0, so x' = 0.0 + (omega (b - 0.0)) / a_ii -- bit-identical to
 // the full sweep without reading the matrix or x.
-template <int BP>
-__global__ void __launch_bounds__(kBlock) k_sweep_zero(int n, int nrhs,
-                                                       const double* __restrict__ diag,
-                                                       const double* __restrict__ b,
-                                                       double* __restrict__ xo, double omega) {
-    const int64_t t = gtid();
-    const int64_t row = t / BP;
-    const int lane = static_cast<int>(t % BP);
-    if (row >= n || lane >= nrhs) return;
-    const int64_t o = row * nrhs + lane;
-    xo[o] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, __dsub_rn(b[o], 0.0)), diag[row]));
+template <int BP, int RPT>
+__global__ void __launch_bounds__(kBlock) k_sweep_zero(int n, int nrhs, const double* __restrict__ diag,
+                                                       const double* __restrict__ b, double* __restrict__ xo,
+                                                       double omega) {
+    ROW_SETUP();
+    if (r >= n || lane0 >= nrhs) return;
+    const int64_t o = r * nrhs + lane0;
+    double bo[RPT], out[RPT];
+    ldv<RPT>(b + o, bo);
+    const double dg = diag[r];
+#pragma unroll
+    for (int l = 0; l < RPT; ++l) out[l] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, __dsub_rn(bo[l], 0.0)), dg));
+    stv<RPT>(xo + o, out);
 }
 
 // r = b - A x (multigrid.cpp:263-265 / 317-318); optionally stores r and/or
 // emits per-CTA partial sums of r^2 for the residual norm.
-template <int BP, bool STORE>
-__global__ void __launch_bounds__(kBlock, 4) k_residual(int n, int nrhs, const int* __restrict__ rp,
-                                                     const int* __restrict__ ci,
-                                                     const double* __restrict__ v,
-                                                     const int* __restrict__ rowid,
-                                                     const double* __restrict__ x,
-                                                     const double* __restrict__ b,
-                                                     double* __restrict__ r,
-                                                     double* __restrict__ partial) {
-    const int64_t t = gtid();
-    const int64_t q = t / BP;
-    const int lane = static_cast<int>(t % BP);
-    const bool valid = q < n && lane < nrhs;
-    double rv = 0.0;
+template <int BP, int RPT, bool STORE>
+__global__ void __launch_bounds__(kBlock, 2) k_residual(int n, int nrhs, const int* __restrict__ rp,
+                                                        const int* __restrict__ ci, const double* __restrict__ v,
+                                                        const int* __restrict__ rowid,
+                                                        const double* __restrict__ x,
+                                                        const double* __restrict__ b, double* __restrict__ rout,
+                                                        double* __restrict__ partial) {
+    ROW_SETUP();
+    const bool valid = r < n && lane0 < nrhs;
+    double rv[RPT];
+#pragma unroll
+    for (int l = 0; l < RPT; ++l) rv[l] = 0.0;
     if (valid) {
-        const int64_t row = rowid ? rowid[q] : q;
-        const int k0 = rp[q], len = rp[q + 1] - k0;
-        const int64_t o = row * nrhs + lane;
-        const double bo = b[o];
-        const double s = row_dot<false>(k0, len, ci, v, x, nrhs, lane, row, nullptr, nullptr);
-        rv = __dsub_rn(bo, s);
-        if (STORE) r[o] = rv;
+        const int64_t row = rowid ? rowid[r] : r;
+        const int64_t o = row * nrhs + lane0;
+        double bo[RPT], s[RPT], dummy[RPT];
+        ldv<RPT>(b + o, bo);
+        const int k0 = rp[r];
+        row_dot<RPT, false>(k0, rp[r + 1] - k0, ci, v, x, nrhs, lane0, row, s, nullptr, dummy);
+#pragma unroll
+        for (int l = 0; l < RPT; ++l) rv[l] = __dsub_rn(bo[l], s[l]);
+        if (STORE) stv<RPT>(rout + o, rv);
     }
-    if (partial) block_partial<BP>(valid ? __dmul_rn(rv, rv) : 0.0, partial);
+    if (partial) {
+        double sq[RPT];
+#pragma unroll
+        for (int l = 0; l < RPT; ++l) sq[l] = __dmul_rn(rv[l], rv[l]);
+        block_partial<BP, RPT>(sq, partial);
+    }
 }
 
 // y = A x over CSR rows (SparseOperator::apply); zero_rows: extension x1
 // (coarse RHS cleared on Dirichlet vertices after restriction).
-template <int BP>
-__global__ void __launch_bounds__(kBlock) k_spmv(int nrows, int nrhs, const int* __restrict__ rp,
-                                                 const int* __restrict__ ci,
-                                                 const double* __restrict__ v,
-                                                 const int* __restrict__ rowid,
-                                                 const double* __restrict__ x,
-                                                 double* __restrict__ y,
-                                                 const int* __restrict__ zero_rows) {
-    const int64_t t = gtid();
-    const int64_t r = t / BP;
-    const int lane = static_cast<int>(t % BP);
-    if (r >= nrows || lane >= nrhs) return;
+template <int BP, int RPT>
+__global__ void __launch_bounds__(kBlock, 2) k_spmv(int nrows, int nrhs, const int* __restrict__ rp,
+                                                    const int* __restrict__ ci, const double* __restrict__ v,
+                                                    const int* __restrict__ rowid, const double* __restrict__ x,
+                                                    double* __restrict__ y, const int* __restrict__ zero_rows) {
+    ROW_SETUP();
+    if (r >= nrows || lane0 >= nrhs) return;
     const int64_t row = rowid ? rowid[r] : r;
+    double s[RPT], dummy[RPT];
     const int k0 = rp[r];
-    double s = row_dot<false>(k0, rp[r + 1] - k0, ci, v, x, nrhs, lane, row, nullptr, nullptr);
-    if (zero_rows && zero_rows[row]) s = 0.0;
-    y[row * nrhs + lane] = s;
+    row_dot<RPT, false>(k0, rp[r + 1] - k0, ci, v, x, nrhs, lane0, row, s, nullptr, dummy);
+    if (zero_rows && zero_rows[row]) {
+#pragma unroll
+        for (int l = 0; l < RPT; ++l) s[l] = 0.0;
+    }
+    stv<RPT>(y + row * nrhs + lane0, s);
 }
 
 // x_f += P x_c (multigrid.cpp:277-280); each fine row owns its entry, so the
 // update is in place.
-template <int BP>
-__global__ void __launch_bounds__(kBlock) k_prolong_add(int n, int nrhs, const int* __restrict__ rp,
-                                                        const int* __restrict__ ci,
-                                                        const double* __restrict__ v,
-                                                        const int* __restrict__ rowid,
-                                                        const double* __restrict__ xc,
-                                                        double* __restrict__ xf) {
-    const int64_t t = gtid();
-    const int64_t r = t / BP;
-    const int lane = static_cast<int>(t % BP);
-    if (r >= n || lane >= nrhs) return;
+template <int BP, int RPT>
+__global__ void __launch_bounds__(kBlock, 2) k_prolong_add(int n, int nrhs, const int* __restrict__ rp,
+                                                           const int* __restrict__ ci,
+                                                           const double* __restrict__ v,
+                                                           const int* __restrict__ rowid,
+                                                           const double* __restrict__ xc,
+                                                           double* __restrict__ xf) {
+    ROW_SETUP();
+    if (r >= n || lane0 >= nrhs) return;
     const int64_t row = rowid ? rowid[r] : r;
-    const int64_t o = row * nrhs + lane;
-    const double xo = xf[o];
+    const int64_t o = row * nrhs + lane0;
+    double xo[RPT], s[RPT], dummy[RPT];
+    ldv<RPT>(xf + o, xo);
     const int k0 = rp[r];
-    const double s = row_dot<false>(k0, rp[r + 1] - k0, ci, v, xc, nrhs, lane, row, nullptr, nullptr);
-    xf[o] = __dadd_rn(xo, s);
+    row_dot<RPT, false>(k0, rp[r + 1] - k0, ci, v, xc, nrhs, lane0, row, s, nullptr, dummy);
+#pragma unroll
+    for (int l = 0; l < RPT; ++l) xo[l] = __dadd_rn(xo[l], s[l]);
+    stv<RPT>(xf + o, xo);
 }
 
 // partials of b_i^2
-template <int BP>
+template <int BP, int RPT>
 __global__ void __launch_bounds__(kBlock) k_sumsq(int n, int nrhs, const double* __restrict__ b,
                                                   double* __restrict__ partial) {
-    const int64_t t = gtid();
-    const int64_t row = t / BP;
-    const int lane = static_cast<int>(t % BP);
-    const bool valid = row < n && lane < nrhs;
-    const double val = valid ? b[row * nrhs + lane] : 0.0;
-    block_partial<BP>(__dmul_rn(val, val), partial);
+    ROW_SETUP();
+    double sq[RPT];
+#pragma unroll
+    for (int l = 0; l < RPT; ++l) sq[l] = 0.0;
+    if (r < n && lane0 < nrhs) {
+        double bv[RPT];
+        ldv<RPT>(b + r * nrhs + lane0, bv);
+#pragma unroll
+        for (int l = 0; l < RPT; ++l) sq[l] = __dmul_rn(bv[l], bv[l]);
+    }
+    block_partial<BP, RPT>(sq, partial);
 }
 
 // Partials are folded by repeated fixed-shape block reductions (each CTA folds
@@ -228,7 +284,8 @@ __global__ void __launch_bounds__(kBlock) k_fold(int64_t nrows, const double* __
     const int64_t t = gtid();
     const int64_t row = t / BP;
     const int lane = static_cast<int>(t % BP);
-    block_partial<BP>(row < nrows ? in[row * BP + lane] : 0.0, out);
+    const double val[1] = {row < nrows ? in[row * BP + lane] : 0.0};
+    block_partial<BP, 1>(val, out);
 }
 
 __global__ void k_finalize(int nrhs, const double* __restrict__ tot, double* __restrict__ out, int mode,
@@ -431,14 +488,20 @@ inline int bp_of(int nrhs) {
     return bp;
 }
 
-#define DISPATCH_BP(bp, ...)                           \
-    switch (bp) {                                      \
-        case 1: { constexpr int BP = 1; __VA_ARGS__; break; }   \
-        case 2: { constexpr int BP = 2; __VA_ARGS__; break; }   \
-        case 4: { constexpr int BP = 4; __VA_ARGS__; break; }   \
-        case 8: { constexpr int BP = 8; __VA_ARGS__; break; }   \
-        case 16: { constexpr int BP = 16; __VA_ARGS__; break; } \
-        default: { constexpr int BP = 32; __VA_ARGS__; break; } \
+// (BP, RPT) instantiations: vector mapping when nrhs == BP >= 2.
+#define DISPATCH_BP(bp, ...)                                              \
+    switch (bp) {                                                         \
+        case 1: { constexpr int BP = 1, RPT = 1; __VA_ARGS__; break; }    \
+        case 2: { constexpr int BP = 2, RPT = 1; __VA_ARGS__; break; }    \
+        case 4: { constexpr int BP = 4, RPT = 1; __VA_ARGS__; break; }    \
+        case 8: { constexpr int BP = 8, RPT = 1; __VA_ARGS__; break; }    \
+        case 16: { constexpr int BP = 16, RPT = 1; __VA_ARGS__; break; }  \
+        case 32: { constexpr int BP = 32, RPT = 1; __VA_ARGS__; break; }  \
+        case -2: { constexpr int BP = 2, RPT = 2; __VA_ARGS__; break; }   \
+        case -4: { constexpr int BP = 4, RPT = 4; __VA_ARGS__; break; }   \
+        case -8: { constexpr int BP = 8, RPT = 4; __VA_ARGS__; break; }   \
+        case -16: { constexpr int BP = 16, RPT = 4; __VA_ARGS__; break; } \
+        default: { constexpr int BP = 32, RPT = 4; __VA_ARGS__; break; }  \
     }
 
 enum Cls { kFineSweep = 0, kFineResidual = 1, kRestrict = 2, kProlong = 3, kCoarseLevels = 4,
@@ -448,11 +511,19 @@ struct Driver {
     decmg_gpu_ctx* c;
     int nrhs, bp;
     const double* b0;  // level-0 right-hand side
+    int key = 0;       // DISPATCH_BP key of the row kernels (-bp: vector mapping)
+    int tpr = 1;       // threads per row
+
+    void init() {
+        const bool vec = nrhs == bp && bp >= 2;
+        key = vec ? -bp : bp;
+        tpr = vec ? bp / (bp < 4 ? bp : 4) : bp;
+    }
 
     const double* bptr(int k) const { return k == 0 ? b0 : c->lv[k].b; }
     static double* xcur(Level& L) { return L.x[L.cur]; }
 
-    unsigned rows_grid(int n) const { return grid_for(static_cast<int64_t>(n) * bp, kBlock); }
+    unsigned rows_grid(int n) const { return grid_for(static_cast<int64_t>(n) * tpr, kBlock); }
 
     Status ensure_x(int k) {
         Level& L = c->lv[k];
@@ -475,14 +546,14 @@ struct Driver {
             if (L.x_zero) {
                 const double bytes = 8.0 * L.nv + 16.0 * L.nv * R;
                 DG_TRY(launch(c, k == 0 ? kFineSweep : kCoarseLevels, bytes, [&] {
-                    DISPATCH_BP(bp, k_sweep_zero<BP><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+                    DISPATCH_BP(key, k_sweep_zero<BP, RPT><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
                                         L.nv, nrhs, L.diag, b, xo, plan.omega));
                 }));
             } else {
                 const double bytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
                 const double* x = xcur(L);
                 DG_TRY(launch(c, k == 0 ? kFineSweep : kCoarseLevels, bytes, [&] {
-                    DISPATCH_BP(bp, k_sweep<BP><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+                    DISPATCH_BP(key, k_sweep<BP, RPT><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
                                         L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b, xo, plan.omega));
                 }));
             }
@@ -502,13 +573,13 @@ struct Driver {
         const double* b = bptr(k);
         const double rbytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
         DG_TRY(launch(c, k == 0 ? kFineResidual : kCoarseLevels, rbytes, [&] {
-            DISPATCH_BP(bp, (k_residual<BP, true><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+            DISPATCH_BP(key, (k_residual<BP, RPT, true><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
                                 L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b, c->r, nullptr)));
         }));
         const double tbytes = 12.0 * L.nnzR + 4.0 * (C.nv + 1) + 8.0 * L.nv * R + 8.0 * C.nv * R;
         const int* zr = c->dirichlet ? C.bd : nullptr;
         DG_TRY(launch(c, k == 0 ? kRestrict : kCoarseLevels, tbytes, [&] {
-            DISPATCH_BP(bp, k_spmv<BP><<<rows_grid(C.nv), kBlock, 0, c->stream>>>(
+            DISPATCH_BP(key, k_spmv<BP, RPT><<<rows_grid(C.nv), kBlock, 0, c->stream>>>(
                                 C.nv, nrhs, L.Ro_rp, L.Ro_ci, L.Ro_v, C.ord, c->r, C.b, zr));
         }));
         return Status::Ok();
@@ -525,7 +596,7 @@ struct Driver {
         const double* xc = xcur(C);
         double* xf = xcur(L);
         DG_TRY(launch(c, k == 0 ? kProlong : kCoarseLevels, bytes, [&] {
-            DISPATCH_BP(bp, k_prolong_add<BP><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+            DISPATCH_BP(key, k_prolong_add<BP, RPT><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
                                 L.nv, nrhs, L.Po_rp, L.Po_ci, L.Po_v, L.ord, xc, xf));
         }));
         return Status::Ok();
@@ -592,7 +663,7 @@ struct Driver {
     Status sumsq(const double* v, double* out, int mode) {
         const int n = c->lv[0].nv;
         DG_TRY(launch(c, kNorms, 8.0 * n * nrhs, [&] {
-            DISPATCH_BP(bp, k_sumsq<BP><<<rows_grid(n), kBlock, 0, c->stream>>>(n, nrhs, v, c->red));
+            DISPATCH_BP(key, k_sumsq<BP, RPT><<<rows_grid(n), kBlock, 0, c->stream>>>(n, nrhs, v, c->red));
         }));
         return reduce_partials(partial_blocks(n), out, mode, nullptr);
     }
@@ -604,7 +675,7 @@ struct Driver {
         const double* x = xcur(L);
         const double bytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 16.0 * L.nv * nrhs;
         DG_TRY(launch(c, kFineResidual, bytes, [&] {
-            DISPATCH_BP(bp, (k_residual<BP, false><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+            DISPATCH_BP(key, (k_residual<BP, RPT, false><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
                                 L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b0, nullptr, c->red)));
         }));
         return reduce_partials(partial_blocks(L.nv), hist, 2, denom);
@@ -678,7 +749,14 @@ Status run_cycles(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_
                   int ncycles, double* d_x, double* d_hist) {
     DG_TRY(check_nrhs(c, nrhs));
     if (ncycles < 0) return Status::Err(DECMG_INVALID_ARGUMENT, "CyclePlan: negative cycle count");
-    Driver dr{c, nrhs, bp_of(nrhs), d_b};
+    const double* b_in = d_b;
+    if ((reinterpret_cast<uintptr_t>(d_b) & 15) != 0) {  // vector loads need 16-byte alignment
+        DG_CUDA(cudaMemcpyAsync(c->bproj, d_b, sizeof(double) * c->lv[0].nv * nrhs, cudaMemcpyDeviceToDevice,
+                                c->stream));
+        b_in = c->bproj;
+    }
+    Driver dr{c, nrhs, bp_of(nrhs), b_in};
+    dr.init();
     double* denom = c->dsmall;
     DG_TRY(dr.load_x0(d_x0));
     DG_TRY(dr.make_denom(denom));
@@ -724,6 +802,7 @@ Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, co
     DG_CUDA(cudaMemcpyAsync(c->bproj, d_b, nbytes, cudaMemcpyDeviceToDevice, c->stream));
     if (!c->dirichlet) DG_TRY(project_compatible(c, nrhs, c->bproj));
     Driver dr{c, nrhs, bp_of(nrhs), c->bproj};
+    dr.init();
     double* denom = c->dsmall;
     double* dres = c->dsmall + 256;
     DG_TRY(dr.load_x0(d_x0));
@@ -796,7 +875,7 @@ Status apply_op(decmg_gpu_ctx* c, int level, char op, const double* d_x, double*
         return Status::Err(DECMG_INVALID_ARGUMENT, "apply: unknown operator for this level");
     }
     DG_TRY(launch(c, kNorms, 0.0, [&] {
-        k_spmv<1><<<grid_for(rows, kBlock), kBlock, 0, c->stream>>>(rows, 1, rp, ci, v, nullptr, d_x, d_y, nullptr);
+        k_spmv<1, 1><<<grid_for(rows, kBlock), kBlock, 0, c->stream>>>(rows, 1, rp, ci, v, nullptr, d_x, d_y, nullptr);
     }));
     return Status::Ok();
 }
