@@ -82,6 +82,15 @@ struct Level {
     int* Ro_rp = nullptr;    // coarse rows of R in the coarse level's order
     int* Ro_ci = nullptr;
     double* Ro_v = nullptr;
+    // Padded ELL copies of Lo (width 8), Po (width 2), Ro (width 8) used when
+    // every row fits (nullptr otherwise): row q at [q*W, q*W + W), padding
+    // column -1 after the real entries.
+    int* Le_ci = nullptr;
+    double* Le_v = nullptr;
+    int* Pe_ci = nullptr;
+    double* Pe_v = nullptr;
+    int* Re_ci = nullptr;
+    double* Re_v = nullptr;
     int zero_diag_row = -1;  // first row with L_ii == 0 (-1: none)
     double wtot = 0.0;       // sum of dual areas, sequential (coarse solve)
     // work vectors [nv][max_nrhs]

@@ -83,55 +83,92 @@ __device__ __forceinline__ void block_partial(const double (&v)[RPT], double* pa
 // Row dot product in the reference order (s = 0.0; s += v_k * x[c_k], per
 // lane) with the loads batched for memory-level parallelism: all column
 // indices and values of the row, then all gathers, then the ordered sums.
-// Rows of up to kMaxRow entries (valence <= 7) take the unrolled path; longer
-// rows use the plain loop. DIAG also returns a_ii and x_ii.
+// W = 8 / 2: padded ELL rows (row q at [q*W, q*W+W), padding ci = -1 after
+// the real entries), read with 16-byte vector loads and no row-pointer round
+// trip. W = 0: CSR (rows of up to kMaxRow entries unrolled, longer rows
+// looped). DIAG also returns a_ii and x_ii.
 constexpr int kMaxRow = 8;
-template <int RPT, bool DIAG>
-__device__ __forceinline__ void row_dot(int k0, int len, const int* __restrict__ ci,
-                                        const double* __restrict__ v, const double* __restrict__ x, int nrhs,
-                                        int lane0, int64_t row, double (&s)[RPT], double* d,
-                                        double (&xr)[RPT]) {
+
+template <int W>
+__device__ __forceinline__ void ell_load(const int* __restrict__ eci, const double* __restrict__ ev, int64_t q,
+                                         int (&cc)[kMaxRow], double (&vv)[kMaxRow]) {
+    if constexpr (W == 8) {
+        const int4* cp = reinterpret_cast<const int4*>(eci + q * 8);
+        const int4 c0 = __ldg(cp), c1 = __ldg(cp + 1);
+        cc[0] = c0.x; cc[1] = c0.y; cc[2] = c0.z; cc[3] = c0.w;
+        cc[4] = c1.x; cc[5] = c1.y; cc[6] = c1.z; cc[7] = c1.w;
+        const double2* vp = reinterpret_cast<const double2*>(ev + q * 8);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const double2 t = __ldg(vp + j);
+            vv[2 * j] = t.x;
+            vv[2 * j + 1] = t.y;
+        }
+    } else {  // W == 2
+        const int2 c0 = __ldg(reinterpret_cast<const int2*>(eci + q * 2));
+        const double2 t = __ldg(reinterpret_cast<const double2*>(ev + q * 2));
+        cc[0] = c0.x; cc[1] = c0.y;
+        vv[0] = t.x; vv[1] = t.y;
+#pragma unroll
+        for (int j = 2; j < kMaxRow; ++j) cc[j] = -1;
+    }
+}
+
+template <int RPT, int W, bool DIAG>
+__device__ __forceinline__ void row_dot(const int* __restrict__ rp, const int* __restrict__ ci,
+                                        const double* __restrict__ v, int64_t q,
+                                        const double* __restrict__ x, int nrhs, int lane0, int64_t row,
+                                        double (&s)[RPT], double* d, double (&xr)[RPT]) {
 #pragma unroll
     for (int l = 0; l < RPT; ++l) s[l] = 0.0;
-    if (len <= kMaxRow) {
-        int cc[kMaxRow];
-        double vv[kMaxRow];
-        double xv[kMaxRow][RPT];
+    int cc[kMaxRow];
+    double vv[kMaxRow];
+    int len;
+    if constexpr (W > 0) {
+        ell_load<W>(ci, v, q, cc, vv);
+        len = kMaxRow;
+    } else {
+        const int k0 = rp[q];
+        len = rp[q + 1] - k0;
+        if (len > kMaxRow) {  // long row: plain loop
+            for (int k = k0; k < k0 + len; ++k) {
+                const int c = ci[k];
+                const double a = v[k];
+                double xx[RPT];
+                ldv<RPT>(x + static_cast<int64_t>(c) * nrhs + lane0, xx);
 #pragma unroll
-        for (int j = 0; j < kMaxRow; ++j)
-            if (j < len) {
-                cc[j] = __ldg(ci + k0 + j);
-                vv[j] = __ldg(v + k0 + j);
-            }
+                for (int l = 0; l < RPT; ++l) s[l] = __dadd_rn(s[l], __dmul_rn(a, xx[l]));
+                if (DIAG && c == row) {
+                    *d = a;
 #pragma unroll
-        for (int j = 0; j < kMaxRow; ++j)
-            if (j < len) ldv<RPT>(x + static_cast<int64_t>(cc[j]) * nrhs + lane0, xv[j]);
-#pragma unroll
-        for (int j = 0; j < kMaxRow; ++j)
-            if (j < len) {
-#pragma unroll
-                for (int l = 0; l < RPT; ++l) s[l] = __dadd_rn(s[l], __dmul_rn(vv[j], xv[j][l]));
-                if (DIAG && cc[j] == row) {
-                    *d = vv[j];
-#pragma unroll
-                    for (int l = 0; l < RPT; ++l) xr[l] = xv[j][l];
+                    for (int l = 0; l < RPT; ++l) xr[l] = xx[l];
                 }
             }
-    } else {
-        for (int k = k0; k < k0 + len; ++k) {
-            const int c = ci[k];
-            const double a = v[k];
-            double xx[RPT];
-            ldv<RPT>(x + static_cast<int64_t>(c) * nrhs + lane0, xx);
+            return;
+        }
 #pragma unroll
-            for (int l = 0; l < RPT; ++l) s[l] = __dadd_rn(s[l], __dmul_rn(a, xx[l]));
-            if (DIAG && c == row) {
-                *d = a;
-#pragma unroll
-                for (int l = 0; l < RPT; ++l) xr[l] = xx[l];
-            }
+        for (int j = 0; j < kMaxRow; ++j) {
+            cc[j] = j < len ? __ldg(ci + k0 + j) : -1;
+            if (j < len) vv[j] = __ldg(v + k0 + j);
         }
     }
+    constexpr int MJ = W == 2 ? 2 : kMaxRow;
+    double xv[MJ][RPT];
+#pragma unroll
+    for (int j = 0; j < MJ; ++j)
+        if (cc[j] >= 0) ldv<RPT>(x + static_cast<int64_t>(cc[j]) * nrhs + lane0, xv[j]);
+#pragma unroll
+    for (int j = 0; j < MJ; ++j)
+        if (cc[j] >= 0) {
+#pragma unroll
+            for (int l = 0; l < RPT; ++l) s[l] = __dadd_rn(s[l], __dmul_rn(vv[j], xv[j][l]));
+            if (DIAG && cc[j] == row) {
+                *d = vv[j];
+#pragma unroll
+                for (int l = 0; l < RPT; ++l) xr[l] = xv[j][l];
+            }
+        }
+    (void)len;
 }
 
 #define ROW_SETUP()                                        \
@@ -143,7 +180,7 @@ __device__ __forceinline__ void row_dot(int k0, int len, const int* __restrict__
 // jacobi_sweep (multigrid.cpp:36-56): s = A x (CSR order),
 // x' = x + (omega (b - s)) / a_ii. x is read entirely before any write
 // (ping-pong buffers), as in the reference, where A.apply fills scratch first.
-template <int BP, int RPT>
+template <int BP, int RPT, int W>
 __global__ void __launch_bounds__(kBlock, 2) k_sweep(int n, int nrhs, const int* __restrict__ rp,
                                                      const int* __restrict__ ci, const double* __restrict__ v,
                                                      const int* __restrict__ rowid, const double* __restrict__ x,
@@ -155,9 +192,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_sweep(int n, int nrhs, const int*
     const int64_t o = row * nrhs + lane0;
     double bo[RPT], s[RPT], xr[RPT], out[RPT];
     ldv<RPT>(b + o, bo);
-    const int k0 = rp[r];
     double d = 0.0;
-    row_dot<RPT, true>(k0, rp[r + 1] - k0, ci, v, x, nrhs, lane0, row, s, &d, xr);
+    row_dot<RPT, W, true>(rp, ci, v, r, x, nrhs, lane0, row, s, &d, xr);
 #pragma unroll
     for (int l = 0; l < RPT; ++l) out[l] = __dadd_rn(xr[l], __ddiv_rn(__dmul_rn(omega, __dsub_rn(bo[l], s[l])), d));
     stv<RPT>(xo + o, out);
@@ -183,7 +219,7 @@ __global__ void __launch_bounds__(kBlock) k_sweep_zero(int n, int nrhs, const do
 
 // r = b - A x (multigrid.cpp:263-265 / 317-318); optionally stores r and/or
 // emits per-CTA partial sums of r^2 for the residual norm.
-template <int BP, int RPT, bool STORE>
+template <int BP, int RPT, int W, bool STORE>
 __global__ void __launch_bounds__(kBlock, 2) k_residual(int n, int nrhs, const int* __restrict__ rp,
                                                         const int* __restrict__ ci, const double* __restrict__ v,
                                                         const int* __restrict__ rowid,
@@ -200,8 +236,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_residual(int n, int nrhs, const i
         const int64_t o = row * nrhs + lane0;
         double bo[RPT], s[RPT], dummy[RPT];
         ldv<RPT>(b + o, bo);
-        const int k0 = rp[r];
-        row_dot<RPT, false>(k0, rp[r + 1] - k0, ci, v, x, nrhs, lane0, row, s, nullptr, dummy);
+        row_dot<RPT, W, false>(rp, ci, v, r, x, nrhs, lane0, row, s, nullptr, dummy);
 #pragma unroll
         for (int l = 0; l < RPT; ++l) rv[l] = __dsub_rn(bo[l], s[l]);
         if (STORE) stv<RPT>(rout + o, rv);
@@ -216,7 +251,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_residual(int n, int nrhs, const i
 
 // y = A x over CSR rows (SparseOperator::apply); zero_rows: extension x1
 // (coarse RHS cleared on Dirichlet vertices after restriction).
-template <int BP, int RPT>
+template <int BP, int RPT, int W>
 __global__ void __launch_bounds__(kBlock, 2) k_spmv(int nrows, int nrhs, const int* __restrict__ rp,
                                                     const int* __restrict__ ci, const double* __restrict__ v,
                                                     const int* __restrict__ rowid, const double* __restrict__ x,
@@ -225,8 +260,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_spmv(int nrows, int nrhs, const i
     if (r >= nrows || lane0 >= nrhs) return;
     const int64_t row = rowid ? rowid[r] : r;
     double s[RPT], dummy[RPT];
-    const int k0 = rp[r];
-    row_dot<RPT, false>(k0, rp[r + 1] - k0, ci, v, x, nrhs, lane0, row, s, nullptr, dummy);
+    row_dot<RPT, W, false>(rp, ci, v, r, x, nrhs, lane0, row, s, nullptr, dummy);
     if (zero_rows && zero_rows[row]) {
 #pragma unroll
         for (int l = 0; l < RPT; ++l) s[l] = 0.0;
@@ -236,7 +270,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_spmv(int nrows, int nrhs, const i
 
 // x_f += P x_c (multigrid.cpp:277-280); each fine row owns its entry, so the
 // update is in place.
-template <int BP, int RPT>
+template <int BP, int RPT, int W>
 __global__ void __launch_bounds__(kBlock, 2) k_prolong_add(int n, int nrhs, const int* __restrict__ rp,
                                                            const int* __restrict__ ci,
                                                            const double* __restrict__ v,
@@ -249,8 +283,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_prolong_add(int n, int nrhs, cons
     const int64_t o = row * nrhs + lane0;
     double xo[RPT], s[RPT], dummy[RPT];
     ldv<RPT>(xf + o, xo);
-    const int k0 = rp[r];
-    row_dot<RPT, false>(k0, rp[r + 1] - k0, ci, v, xc, nrhs, lane0, row, s, nullptr, dummy);
+    row_dot<RPT, W, false>(rp, ci, v, r, xc, nrhs, lane0, row, s, nullptr, dummy);
 #pragma unroll
     for (int l = 0; l < RPT; ++l) xo[l] = __dadd_rn(xo[l], s[l]);
     stv<RPT>(xf + o, xo);
@@ -553,8 +586,12 @@ struct Driver {
                 const double bytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
                 const double* x = xcur(L);
                 DG_TRY(launch(c, k == 0 ? kFineSweep : kCoarseLevels, bytes, [&] {
-                    DISPATCH_BP(key, k_sweep<BP, RPT><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                        L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b, xo, plan.omega));
+                    if (L.Le_ci)
+                        DISPATCH_BP(key, (k_sweep<BP, RPT, 8><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+                                            L.nv, nrhs, nullptr, L.Le_ci, L.Le_v, L.ord, x, b, xo, plan.omega)))
+                    else
+                        DISPATCH_BP(key, (k_sweep<BP, RPT, 0><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+                                            L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b, xo, plan.omega)))
                 }));
             }
             L.cur ^= 1;
@@ -573,14 +610,22 @@ struct Driver {
         const double* b = bptr(k);
         const double rbytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
         DG_TRY(launch(c, k == 0 ? kFineResidual : kCoarseLevels, rbytes, [&] {
-            DISPATCH_BP(key, (k_residual<BP, RPT, true><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b, c->r, nullptr)));
+            if (L.Le_ci)
+                DISPATCH_BP(key, (k_residual<BP, RPT, 8, true><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+                                    L.nv, nrhs, nullptr, L.Le_ci, L.Le_v, L.ord, x, b, c->r, nullptr)))
+            else
+                DISPATCH_BP(key, (k_residual<BP, RPT, 0, true><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+                                    L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b, c->r, nullptr)))
         }));
         const double tbytes = 12.0 * L.nnzR + 4.0 * (C.nv + 1) + 8.0 * L.nv * R + 8.0 * C.nv * R;
         const int* zr = c->dirichlet ? C.bd : nullptr;
         DG_TRY(launch(c, k == 0 ? kRestrict : kCoarseLevels, tbytes, [&] {
-            DISPATCH_BP(key, k_spmv<BP, RPT><<<rows_grid(C.nv), kBlock, 0, c->stream>>>(
-                                C.nv, nrhs, L.Ro_rp, L.Ro_ci, L.Ro_v, C.ord, c->r, C.b, zr));
+            if (L.Re_ci)
+                DISPATCH_BP(key, (k_spmv<BP, RPT, 8><<<rows_grid(C.nv), kBlock, 0, c->stream>>>(
+                                    C.nv, nrhs, nullptr, L.Re_ci, L.Re_v, C.ord, c->r, C.b, zr)))
+            else
+                DISPATCH_BP(key, (k_spmv<BP, RPT, 0><<<rows_grid(C.nv), kBlock, 0, c->stream>>>(
+                                    C.nv, nrhs, L.Ro_rp, L.Ro_ci, L.Ro_v, C.ord, c->r, C.b, zr)))
         }));
         return Status::Ok();
     }
@@ -596,8 +641,12 @@ struct Driver {
         const double* xc = xcur(C);
         double* xf = xcur(L);
         DG_TRY(launch(c, k == 0 ? kProlong : kCoarseLevels, bytes, [&] {
-            DISPATCH_BP(key, k_prolong_add<BP, RPT><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                L.nv, nrhs, L.Po_rp, L.Po_ci, L.Po_v, L.ord, xc, xf));
+            if (L.Pe_ci)
+                DISPATCH_BP(key, (k_prolong_add<BP, RPT, 2><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+                                    L.nv, nrhs, nullptr, L.Pe_ci, L.Pe_v, L.ord, xc, xf)))
+            else
+                DISPATCH_BP(key, (k_prolong_add<BP, RPT, 0><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+                                    L.nv, nrhs, L.Po_rp, L.Po_ci, L.Po_v, L.ord, xc, xf)))
         }));
         return Status::Ok();
     }
@@ -675,8 +724,12 @@ struct Driver {
         const double* x = xcur(L);
         const double bytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 16.0 * L.nv * nrhs;
         DG_TRY(launch(c, kFineResidual, bytes, [&] {
-            DISPATCH_BP(key, (k_residual<BP, RPT, false><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b0, nullptr, c->red)));
+            if (L.Le_ci)
+                DISPATCH_BP(key, (k_residual<BP, RPT, 8, false><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+                                    L.nv, nrhs, nullptr, L.Le_ci, L.Le_v, L.ord, x, b0, nullptr, c->red)))
+            else
+                DISPATCH_BP(key, (k_residual<BP, RPT, 0, false><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+                                    L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b0, nullptr, c->red)))
         }));
         return reduce_partials(partial_blocks(L.nv), hist, 2, denom);
     }
@@ -875,7 +928,7 @@ Status apply_op(decmg_gpu_ctx* c, int level, char op, const double* d_x, double*
         return Status::Err(DECMG_INVALID_ARGUMENT, "apply: unknown operator for this level");
     }
     DG_TRY(launch(c, kNorms, 0.0, [&] {
-        k_spmv<1, 1><<<grid_for(rows, kBlock), kBlock, 0, c->stream>>>(rows, 1, rp, ci, v, nullptr, d_x, d_y, nullptr);
+        k_spmv<1, 1, 0><<<grid_for(rows, kBlock), kBlock, 0, c->stream>>>(rows, 1, rp, ci, v, nullptr, d_x, d_y, nullptr);
     }));
     return Status::Ok();
 }

@@ -504,6 +504,23 @@ __global__ void k_perm_fill(int n, const int* __restrict__ ord, const int* __res
     }
 }
 
+__global__ void k_row_maxlen(int n, const int* __restrict__ rp, int* mx) {
+    const int64_t q = gtid();
+    if (q >= n) return;
+    atomicMax(mx, rp[q + 1] - rp[q]);
+}
+
+__global__ void k_ell_fill(int n, int W, const int* __restrict__ rp, const int* __restrict__ ci,
+                           const double* __restrict__ v, int* __restrict__ eci, double* __restrict__ ev) {
+    const int64_t q = gtid();
+    if (q >= n) return;
+    const int k0 = rp[q], len = rp[q + 1] - k0;
+    for (int j = 0; j < W; ++j) {
+        eci[q * W + j] = j < len ? ci[k0 + j] : -1;
+        ev[q * W + j] = j < len ? v[k0 + j] : 0.0;
+    }
+}
+
 // ------------------------------------------------------------ helpers ------
 struct TmpPool {
     cudaStream_t s;
@@ -724,6 +741,27 @@ Status permute_rows(decmg_gpu_ctx* c, int nrows, const int* ord, const int* rp, 
     return Status::Ok();
 }
 
+// Padded ELL copy of a row-ordered CSR when every row has <= W entries.
+Status build_ell(decmg_gpu_ctx* c, int nrows, const int* rp, const int* ci, const double* v, int W, int** eci,
+                 double** ev) {
+    TmpPool tp(c->stream);
+    int* mx;
+    DG_TRY(tp.get(&mx, 1));
+    DG_CUDA(cudaMemsetAsync(mx, 0, sizeof(int), c->stream));
+    LAUNCH(4, nrows, k_row_maxlen, nrows, rp, mx);
+    int h = 0;
+    DG_TRY(read_int(c, mx, &h));
+    if (h > W) {
+        *eci = nullptr;
+        *ev = nullptr;
+        return Status::Ok();
+    }
+    DG_TRY(dalloc(c, eci, static_cast<size_t>(nrows) * W));
+    DG_TRY(dalloc(c, ev, static_cast<size_t>(nrows) * W));
+    LAUNCH(4, nrows, k_ell_fill, nrows, W, rp, ci, v, *eci, *ev);
+    return Status::Ok();
+}
+
 // Row orders for every level except the coarsest (its CG runs sequentially
 // in the reference order), then the reordered L, P and R.
 Status build_orders(decmg_gpu_ctx* c) {
@@ -750,6 +788,13 @@ Status build_orders(decmg_gpu_ctx* c) {
                 m.Ro_rp = m.R_rp; m.Ro_ci = m.R_ci; m.Ro_v = m.R_v;
             }
         }
+    }
+    for (int k = 0; k + 1 < L; ++k) {  // the coarsest level only runs the sequential CG
+        Level& m = c->lv[k];
+        const Level& cm = c->lv[k + 1];
+        DG_TRY(build_ell(c, m.nv, m.Lo_rp, m.Lo_ci, m.Lo_v, 8, &m.Le_ci, &m.Le_v));
+        DG_TRY(build_ell(c, m.nv, m.Po_rp, m.Po_ci, m.Po_v, 2, &m.Pe_ci, &m.Pe_v));
+        DG_TRY(build_ell(c, cm.nv, m.Ro_rp, m.Ro_ci, m.Ro_v, 8, &m.Re_ci, &m.Re_v));
     }
     DG_CUDA(cudaStreamSynchronize(c->stream));
     return Status::Ok();
