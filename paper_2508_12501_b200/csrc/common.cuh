@@ -137,6 +137,7 @@ struct decmg_gpu_ctx {
     double* io_x0 = nullptr;
     double* io_x = nullptr;
     int64_t launch_count = 0;
+    int rpt = 4;                // right-hand sides per thread in the vector mapping (env DECMG_RPT)
     decmg_gpu::Timing timing;
     std::string err;
     std::vector<void*> allocations;

@@ -521,20 +521,34 @@ inline int bp_of(int nrhs) {
     return bp;
 }
 
-// (BP, RPT) instantiations: vector mapping when nrhs == BP >= 2.
-#define DISPATCH_BP(bp, ...)                                              \
-    switch (bp) {                                                         \
-        case 1: { constexpr int BP = 1, RPT = 1; __VA_ARGS__; break; }    \
-        case 2: { constexpr int BP = 2, RPT = 1; __VA_ARGS__; break; }    \
-        case 4: { constexpr int BP = 4, RPT = 1; __VA_ARGS__; break; }    \
-        case 8: { constexpr int BP = 8, RPT = 1; __VA_ARGS__; break; }    \
-        case 16: { constexpr int BP = 16, RPT = 1; __VA_ARGS__; break; }  \
-        case 32: { constexpr int BP = 32, RPT = 1; __VA_ARGS__; break; }  \
-        case -2: { constexpr int BP = 2, RPT = 2; __VA_ARGS__; break; }   \
-        case -4: { constexpr int BP = 4, RPT = 4; __VA_ARGS__; break; }   \
-        case -8: { constexpr int BP = 8, RPT = 4; __VA_ARGS__; break; }   \
-        case -16: { constexpr int BP = 16, RPT = 4; __VA_ARGS__; break; } \
-        default: { constexpr int BP = 32, RPT = 4; __VA_ARGS__; break; }  \
+// (BP, RPT) instantiations, key = 10 * BP + RPT. RPT > 1 (16-byte vector
+// mapping) only when nrhs == BP >= 2.
+#define DISPATCH_BP(key, ...)                                                    \
+    switch (key) {                                                              \
+        case 11: { constexpr int BP = 1, RPT = 1; __VA_ARGS__; break; }         \
+        case 21: { constexpr int BP = 2, RPT = 1; __VA_ARGS__; break; }         \
+        case 41: { constexpr int BP = 4, RPT = 1; __VA_ARGS__; break; }         \
+        case 81: { constexpr int BP = 8, RPT = 1; __VA_ARGS__; break; }         \
+        case 161: { constexpr int BP = 16, RPT = 1; __VA_ARGS__; break; }       \
+        case 321: { constexpr int BP = 32, RPT = 1; __VA_ARGS__; break; }       \
+        case 22: { constexpr int BP = 2, RPT = 2; __VA_ARGS__; break; }         \
+        case 42: { constexpr int BP = 4, RPT = 2; __VA_ARGS__; break; }         \
+        case 44: { constexpr int BP = 4, RPT = 4; __VA_ARGS__; break; }         \
+        case 82: { constexpr int BP = 8, RPT = 2; __VA_ARGS__; break; }         \
+        case 84: { constexpr int BP = 8, RPT = 4; __VA_ARGS__; break; }         \
+        case 162: { constexpr int BP = 16, RPT = 2; __VA_ARGS__; break; }       \
+        case 164: { constexpr int BP = 16, RPT = 4; __VA_ARGS__; break; }       \
+        case 322: { constexpr int BP = 32, RPT = 2; __VA_ARGS__; break; }       \
+        default: { constexpr int BP = 32, RPT = 4; __VA_ARGS__; break; }        \
+    }
+#define DISPATCH_B1(bp, ...)                                                    \
+    switch (bp) {                                                               \
+        case 1: { constexpr int BP = 1; __VA_ARGS__; break; }                   \
+        case 2: { constexpr int BP = 2; __VA_ARGS__; break; }                   \
+        case 4: { constexpr int BP = 4; __VA_ARGS__; break; }                   \
+        case 8: { constexpr int BP = 8; __VA_ARGS__; break; }                   \
+        case 16: { constexpr int BP = 16; __VA_ARGS__; break; }                 \
+        default: { constexpr int BP = 32; __VA_ARGS__; break; }                 \
     }
 
 enum Cls { kFineSweep = 0, kFineResidual = 1, kRestrict = 2, kProlong = 3, kCoarseLevels = 4,
@@ -549,8 +563,9 @@ struct Driver {
 
     void init() {
         const bool vec = nrhs == bp && bp >= 2;
-        key = vec ? -bp : bp;
-        tpr = vec ? bp / (bp < 4 ? bp : 4) : bp;
+        int rpt = vec ? (bp < c->rpt ? bp : c->rpt) : 1;
+        key = 10 * bp + rpt;
+        tpr = bp / rpt;
     }
 
     const double* bptr(int k) const { return k == 0 ? b0 : c->lv[k].b; }
@@ -699,7 +714,7 @@ struct Driver {
             const int64_t threads = nrows * bp;
             const unsigned g = grid_for(threads, kBlock);
             DG_TRY(launch(c, kNorms, 8.0 * threads, [&] {
-                DISPATCH_BP(bp, k_fold<BP><<<g, kBlock, 0, c->stream>>>(nrows, in, nxt));
+                DISPATCH_B1(bp, k_fold<BP><<<g, kBlock, 0, c->stream>>>(nrows, in, nxt));
             }));
             nrows = g;
             std::swap(in, nxt);
@@ -838,7 +853,7 @@ Status project_compatible(decmg_gpu_ctx* c, int nrhs, double* d_b) {
     }));
     const unsigned g = grid_for(static_cast<int64_t>(L.nv) * bp, kBlock);
     DG_TRY(launch(c, kNorms, 16.0 * L.nv * nrhs, [&] {
-        DISPATCH_BP(bp, k_project<BP><<<g, kBlock, 0, c->stream>>>(L.nv, nrhs, mean, d_b));
+        DISPATCH_B1(bp, k_project<BP><<<g, kBlock, 0, c->stream>>>(L.nv, nrhs, mean, d_b));
     }));
     return Status::Ok();
 }
