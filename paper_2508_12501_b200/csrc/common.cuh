@@ -91,6 +91,8 @@ struct Level {
     double* Pe_v = nullptr;
     int* Re_ci = nullptr;
     double* Re_v = nullptr;
+    int* Le_row = nullptr;   // original row id per ELL row of Le/Pe (padded, -1 = padding)
+    int* Re_row = nullptr;   // original coarse row id per ELL row of Re
     int zero_diag_row = -1;  // first row with L_ii == 0 (-1: none)
     double wtot = 0.0;       // sum of dual areas, sequential (coarse solve)
     // work vectors [nv][max_nrhs]
@@ -137,7 +139,8 @@ struct decmg_gpu_ctx {
     double* io_x0 = nullptr;
     double* io_x = nullptr;
     int64_t launch_count = 0;
-    int rpt = 4;                // right-hand sides per thread in the vector mapping (env DECMG_RPT)
+    int rpt = 4;
+    int num_sms = 148;                // right-hand sides per thread in the vector mapping (env DECMG_RPT)
     decmg_gpu::Timing timing;
     std::string err;
     std::vector<void*> allocations;

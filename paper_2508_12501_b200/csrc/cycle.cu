@@ -20,6 +20,7 @@
 // Norms and projections use a fixed-shape tree reduction: deterministic run
 // to run, within a few ulps of the reference's blocked sums.
 #include "common.cuh"
+#include "ptx.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -289,6 +290,173 @@ __global__ void __launch_bounds__(kBlock, 2) k_prolong_add(int n, int nrhs, cons
     stv<RPT>(xf + o, xo);
 }
 
+// ------------------------------------------------------------------------
+// Pipelined persistent row kernel (the hot path on ELL levels).
+//
+// One producer thread streams the index tiles of the reordered operator --
+// kPipeRows rows of ELL column indices, values and original row ids -- into a
+// kPipeStages-deep shared-memory ring with TMA bulk copies (cp.async.bulk +
+// mbarrier complete_tx). 256 consumer threads (kPipeRows = 224 / TPR rows per
+// tile, RPT right-hand sides each) read their row's indices from the ring and
+// issue all x gathers at once: the only memory round trip left on a
+// consumer's critical path is the gather itself. Tiles are
+// assigned statically (tile = blockIdx.x + i * gridDim.x), so every result,
+// including the residual-norm partials, is deterministic for a given grid.
+//
+// OP: 0 sweep (jacobi_sweep), 1 residual store, 2 residual norm partials,
+//     3 y = A x with Dirichlet zero rows (restriction), 4 x += P xc (prolong).
+// 7 consumer warps + 1 producer warp: two CTAs per SM put 4 warps on each
+// SM sub-partition, which leaves 128 registers per thread.
+constexpr int kPipeConsumers = 224;
+constexpr int kPipeThreads = kPipeConsumers + 32;
+constexpr int kPipeStages = 4;
+enum { OP_SWEEP = 0, OP_RES_STORE = 1, OP_RES_NORM = 2, OP_SPMV = 3, OP_PROLONG = 4 };
+
+struct PipeArgs {
+    int ntiles, nrhs;
+    const int* eci;
+    const double* ev;
+    const int* ord;     // padded: ntiles * rows_per_tile entries, -1 = padding row
+    const double* x;    // gathered vector
+    const double* b;    // OP_SWEEP / OP_RES_*: right-hand side
+    double* out;        // OP_SWEEP: x'; OP_RES_STORE: r; OP_SPMV: y; OP_PROLONG: x_f (in/out)
+    double* partial;    // OP_RES_NORM
+    const int* zero_rows;
+    double omega;
+};
+
+template <int BP, int RPT, int W>
+struct PipeGeom {
+    static constexpr int TPR = BP / RPT;
+    static constexpr int ROWS = kPipeConsumers / TPR;
+    static constexpr uint32_t CI_BYTES = ROWS * W * 4, V_BYTES = ROWS * W * 8, ORD_BYTES = ROWS * 4;
+    static constexpr uint32_t STAGE_BYTES = V_BYTES + CI_BYTES + ORD_BYTES;
+    static constexpr size_t SMEM = static_cast<size_t>(kPipeStages) * STAGE_BYTES;
+};
+
+template <int BP, int RPT, int W, int OP>
+__global__ void __launch_bounds__(kPipeThreads, 2) k_rowop_pipe(PipeArgs a) {
+    using G = PipeGeom<BP, RPT, W>;
+    constexpr int TPR = G::TPR, ROWS = G::ROWS;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full[kPipeStages], empty[kPipeStages];
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < kPipeStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kPipeConsumers / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int ntiles = a.ntiles;
+    double acc[RPT];
+#pragma unroll
+    for (int l = 0; l < RPT; ++l) acc[l] = 0.0;
+
+    if (tid >= kPipeConsumers) {
+        if (tid == kPipeConsumers) {  // producer
+            int i = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+                const int s = i % kPipeStages;
+                if (i >= kPipeStages) mbar_wait(&empty[s], ((i / kPipeStages) - 1) & 1);
+                unsigned char* st = smem_raw + static_cast<size_t>(s) * G::STAGE_BYTES;
+                mbar_expect_tx(&full[s], G::STAGE_BYTES);
+                tma_bulk_g2s(st, a.ev + static_cast<int64_t>(t) * ROWS * W, G::V_BYTES, &full[s]);
+                tma_bulk_g2s(st + G::V_BYTES, a.eci + static_cast<int64_t>(t) * ROWS * W, G::CI_BYTES, &full[s]);
+                tma_bulk_g2s(st + G::V_BYTES + G::CI_BYTES, a.ord + static_cast<int64_t>(t) * ROWS, G::ORD_BYTES,
+                             &full[s]);
+            }
+        }
+    } else {
+        const int q = tid / TPR;
+        const int lane0 = (tid % TPR) * RPT;
+        const int nrhs = a.nrhs;
+        int i = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            const int s = i % kPipeStages;
+            mbar_wait(&full[s], (i / kPipeStages) & 1);
+            const unsigned char* st = smem_raw + static_cast<size_t>(s) * G::STAGE_BYTES;
+            const double* vs = reinterpret_cast<const double*>(st);
+            const int* cs = reinterpret_cast<const int*>(st + G::V_BYTES);
+            const int* os = reinterpret_cast<const int*>(st + G::V_BYTES + G::CI_BYTES);
+            // indices and values are read straight from the stage (kept until
+            // the tile is done), so registers hold only the gathered x values
+            const int* cq = cs + q * W;
+            const double* vq = vs + q * W;
+            const int row32 = os[q];
+            const bool active = row32 >= 0 && lane0 < nrhs;
+            const int64_t row = row32;
+            const int64_t o = row * nrhs + lane0;
+            double pre[RPT], xv[W][RPT], sum[RPT], xr[RPT], d = 0.0;
+            if (active) {
+                if constexpr (OP == OP_SWEEP || OP == OP_RES_STORE || OP == OP_RES_NORM) ldv<RPT>(a.b + o, pre);
+                if constexpr (OP == OP_PROLONG) ldv<RPT>(a.out + o, pre);
+#pragma unroll
+                for (int j = 0; j < W; ++j) {
+                    const int cj = cq[j];
+                    if (cj >= 0) ldv<RPT>(a.x + static_cast<int64_t>(cj) * nrhs + lane0, xv[j]);
+                }
+#pragma unroll
+                for (int l = 0; l < RPT; ++l) sum[l] = 0.0;
+#pragma unroll
+                for (int j = 0; j < W; ++j) {
+                    const int cj = cq[j];
+                    if (cj >= 0) {
+                        const double vj = vq[j];
+#pragma unroll
+                        for (int l = 0; l < RPT; ++l) sum[l] = __dadd_rn(sum[l], __dmul_rn(vj, xv[j][l]));
+                        if (OP == OP_SWEEP && cj == row32) d = vj;
+                    }
+                }
+                // x_ii: re-read (an L1 hit -- the diagonal gather just brought it in)
+                if constexpr (OP == OP_SWEEP) ldv<RPT>(a.x + o, xr);
+            }
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&empty[s]);  // stage consumed
+            if (!active) continue;
+            double res[RPT];
+#pragma unroll
+            for (int l = 0; l < RPT; ++l) {
+                if constexpr (OP == OP_SWEEP)
+                    res[l] = __dadd_rn(xr[l], __ddiv_rn(__dmul_rn(a.omega, __dsub_rn(pre[l], sum[l])), d));
+                else if constexpr (OP == OP_RES_STORE || OP == OP_RES_NORM)
+                    res[l] = __dsub_rn(pre[l], sum[l]);
+                else if constexpr (OP == OP_PROLONG)
+                    res[l] = __dadd_rn(pre[l], sum[l]);
+                else
+                    res[l] = sum[l];
+            }
+            if constexpr (OP == OP_SPMV) {
+                if (a.zero_rows && a.zero_rows[row]) {
+#pragma unroll
+                    for (int l = 0; l < RPT; ++l) res[l] = 0.0;
+                }
+            }
+            if constexpr (OP == OP_RES_NORM) {
+#pragma unroll
+                for (int l = 0; l < RPT; ++l) acc[l] = __dadd_rn(acc[l], __dmul_rn(res[l], res[l]));
+            } else {
+                stv<RPT>(a.out + o, res);
+            }
+        }
+    }
+    if constexpr (OP == OP_RES_NORM) {
+        // fold the consumers' accumulators: [ROWS][BP] in a fixed tree order
+        __shared__ double sh[kPipeConsumers * RPT];
+        if (tid < kPipeConsumers)
+#pragma unroll
+            for (int l = 0; l < RPT; ++l) sh[tid * RPT + l] = acc[l];
+        __syncthreads();
+        for (int sft = ROWS / 2; sft >= 1; sft >>= 1) {
+            for (int idx = tid; idx < sft * BP; idx += kPipeThreads) sh[idx] = __dadd_rn(sh[idx], sh[idx + sft * BP]);
+            __syncthreads();
+        }
+        for (int idx = tid; idx < BP; idx += kPipeThreads)
+            a.partial[static_cast<int64_t>(blockIdx.x) * BP + idx] = sh[idx];
+    }
+}
+
 // partials of b_i^2
 template <int BP, int RPT>
 __global__ void __launch_bounds__(kBlock) k_sumsq(int n, int nrhs, const double* __restrict__ b,
@@ -348,36 +516,6 @@ __global__ void k_denom(int nrhs, const double* __restrict__ bn, double* __restr
 // copies (cp.async.bulk + mbarrier complete_tx), and warp 0 consumes them.
 constexpr int kProjStages = 4;
 constexpr int kProjRows = 128;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
 
 __global__ void __launch_bounds__(64) k_project_sums(int n, int nrhs, const double* __restrict__ w,
                                                      const double* __restrict__ b,
@@ -573,6 +711,33 @@ struct Driver {
 
     unsigned rows_grid(int n) const { return grid_for(static_cast<int64_t>(n) * tpr, kBlock); }
 
+    // Launch the pipelined persistent row kernel on an ELL operator.
+    // Returns the grid size in *grid (the number of norm partials for OP_RES_NORM).
+    template <int OP, int W>
+    Status pipe(int cls, double bytes, int nrows, const int* eci, const double* ev, const int* erow,
+                const double* x, const double* b, double* out, double* partial, const int* zr, double omega,
+                int* grid = nullptr) {
+        Status st;
+        DISPATCH_BP(key, {
+            using G = PipeGeom<BP, RPT, W>;
+            static_assert(G::ROWS * 4 % 16 == 0 || BP / RPT > 8, "pipe tile");
+            const int ntiles = (nrows + G::ROWS - 1) / G::ROWS;
+            const int g = ntiles < 2 * c->num_sms ? ntiles : 2 * c->num_sms;
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_rowop_pipe<BP, RPT, W, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(G::SMEM));
+                attr = true;
+            }
+            PipeArgs a{ntiles, nrhs, eci, ev, erow, x, b, out, partial, zr, omega};
+            st = launch(c, cls, bytes, [&] {
+                k_rowop_pipe<BP, RPT, W, OP><<<g, kPipeThreads, G::SMEM, c->stream>>>(a);
+            });
+            if (grid) *grid = g;
+        })
+        return st;
+    }
+
     Status ensure_x(int k) {
         Level& L = c->lv[k];
         if (L.x_zero) {
@@ -600,14 +765,15 @@ struct Driver {
             } else {
                 const double bytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
                 const double* x = xcur(L);
-                DG_TRY(launch(c, k == 0 ? kFineSweep : kCoarseLevels, bytes, [&] {
-                    if (L.Le_ci)
-                        DISPATCH_BP(key, (k_sweep<BP, RPT, 8><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                            L.nv, nrhs, nullptr, L.Le_ci, L.Le_v, L.ord, x, b, xo, plan.omega)))
-                    else
+                if (L.Le_ci && tpr <= 8) {
+                    DG_TRY((pipe<OP_SWEEP, 8>(k == 0 ? kFineSweep : kCoarseLevels, bytes, L.nv, L.Le_ci, L.Le_v,
+                                              L.Le_row, x, b, xo, nullptr, nullptr, plan.omega)));
+                } else {
+                    DG_TRY(launch(c, k == 0 ? kFineSweep : kCoarseLevels, bytes, [&] {
                         DISPATCH_BP(key, (k_sweep<BP, RPT, 0><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
                                             L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b, xo, plan.omega)))
-                }));
+                    }));
+                }
             }
             L.cur ^= 1;
             L.x_zero = false;
@@ -624,24 +790,26 @@ struct Driver {
         const double* x = xcur(L);
         const double* b = bptr(k);
         const double rbytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
-        DG_TRY(launch(c, k == 0 ? kFineResidual : kCoarseLevels, rbytes, [&] {
-            if (L.Le_ci)
-                DISPATCH_BP(key, (k_residual<BP, RPT, 8, true><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                    L.nv, nrhs, nullptr, L.Le_ci, L.Le_v, L.ord, x, b, c->r, nullptr)))
-            else
+        if (L.Le_ci && tpr <= 8) {
+            DG_TRY((pipe<OP_RES_STORE, 8>(k == 0 ? kFineResidual : kCoarseLevels, rbytes, L.nv, L.Le_ci, L.Le_v,
+                                          L.Le_row, x, b, c->r, nullptr, nullptr, 0.0)));
+        } else {
+            DG_TRY(launch(c, k == 0 ? kFineResidual : kCoarseLevels, rbytes, [&] {
                 DISPATCH_BP(key, (k_residual<BP, RPT, 0, true><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
                                     L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b, c->r, nullptr)))
-        }));
+            }));
+        }
         const double tbytes = 12.0 * L.nnzR + 4.0 * (C.nv + 1) + 8.0 * L.nv * R + 8.0 * C.nv * R;
         const int* zr = c->dirichlet ? C.bd : nullptr;
-        DG_TRY(launch(c, k == 0 ? kRestrict : kCoarseLevels, tbytes, [&] {
-            if (L.Re_ci)
-                DISPATCH_BP(key, (k_spmv<BP, RPT, 8><<<rows_grid(C.nv), kBlock, 0, c->stream>>>(
-                                    C.nv, nrhs, nullptr, L.Re_ci, L.Re_v, C.ord, c->r, C.b, zr)))
-            else
+        if (L.Re_ci && tpr <= 8) {
+            DG_TRY((pipe<OP_SPMV, 8>(k == 0 ? kRestrict : kCoarseLevels, tbytes, C.nv, L.Re_ci, L.Re_v, L.Re_row,
+                                     c->r, nullptr, C.b, nullptr, zr, 0.0)));
+        } else {
+            DG_TRY(launch(c, k == 0 ? kRestrict : kCoarseLevels, tbytes, [&] {
                 DISPATCH_BP(key, (k_spmv<BP, RPT, 0><<<rows_grid(C.nv), kBlock, 0, c->stream>>>(
                                     C.nv, nrhs, L.Ro_rp, L.Ro_ci, L.Ro_v, C.ord, c->r, C.b, zr)))
-        }));
+            }));
+        }
         return Status::Ok();
     }
 
@@ -655,14 +823,15 @@ struct Driver {
         const double bytes = 12.0 * L.nnzP + 4.0 * (L.nv + 1) + 8.0 * C.nv * R + 16.0 * L.nv * R;
         const double* xc = xcur(C);
         double* xf = xcur(L);
-        DG_TRY(launch(c, k == 0 ? kProlong : kCoarseLevels, bytes, [&] {
-            if (L.Pe_ci)
-                DISPATCH_BP(key, (k_prolong_add<BP, RPT, 2><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                    L.nv, nrhs, nullptr, L.Pe_ci, L.Pe_v, L.ord, xc, xf)))
-            else
+        if (L.Pe_ci && tpr <= 8) {
+            DG_TRY((pipe<OP_PROLONG, 2>(k == 0 ? kProlong : kCoarseLevels, bytes, L.nv, L.Pe_ci, L.Pe_v, L.Le_row,
+                                        xc, nullptr, xf, nullptr, nullptr, 0.0)));
+        } else {
+            DG_TRY(launch(c, k == 0 ? kProlong : kCoarseLevels, bytes, [&] {
                 DISPATCH_BP(key, (k_prolong_add<BP, RPT, 0><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
                                     L.nv, nrhs, L.Po_rp, L.Po_ci, L.Po_v, L.ord, xc, xf)))
-        }));
+            }));
+        }
         return Status::Ok();
     }
 
@@ -738,13 +907,15 @@ struct Driver {
         Level& L = c->lv[0];
         const double* x = xcur(L);
         const double bytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 16.0 * L.nv * nrhs;
+        if (L.Le_ci && tpr <= 8) {
+            int g = 0;
+            DG_TRY((pipe<OP_RES_NORM, 8>(kFineResidual, bytes, L.nv, L.Le_ci, L.Le_v, L.Le_row, x, b0, nullptr,
+                                         c->red, nullptr, 0.0, &g)));
+            return reduce_partials(g, hist, 2, denom);
+        }
         DG_TRY(launch(c, kFineResidual, bytes, [&] {
-            if (L.Le_ci)
-                DISPATCH_BP(key, (k_residual<BP, RPT, 8, false><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                    L.nv, nrhs, nullptr, L.Le_ci, L.Le_v, L.ord, x, b0, nullptr, c->red)))
-            else
-                DISPATCH_BP(key, (k_residual<BP, RPT, 0, false><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                    L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b0, nullptr, c->red)))
+            DISPATCH_BP(key, (k_residual<BP, RPT, 0, false><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
+                                L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b0, nullptr, c->red)))
         }));
         return reduce_partials(partial_blocks(L.nv), hist, 2, denom);
     }

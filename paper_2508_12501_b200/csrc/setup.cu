@@ -510,15 +510,18 @@ __global__ void k_row_maxlen(int n, const int* __restrict__ rp, int* mx) {
     atomicMax(mx, rp[q + 1] - rp[q]);
 }
 
-__global__ void k_ell_fill(int n, int W, const int* __restrict__ rp, const int* __restrict__ ci,
-                           const double* __restrict__ v, int* __restrict__ eci, double* __restrict__ ev) {
+// rows >= n are padding (column -1, row id -1) up to npad
+__global__ void k_ell_fill(int n, int npad, int W, const int* __restrict__ rp, const int* __restrict__ ci,
+                           const double* __restrict__ v, const int* __restrict__ ord, int* __restrict__ eci,
+                           double* __restrict__ ev, int* __restrict__ erow) {
     const int64_t q = gtid();
-    if (q >= n) return;
-    const int k0 = rp[q], len = rp[q + 1] - k0;
+    if (q >= npad) return;
+    const int k0 = q < n ? rp[q] : 0, len = q < n ? rp[q + 1] - k0 : 0;
     for (int j = 0; j < W; ++j) {
         eci[q * W + j] = j < len ? ci[k0 + j] : -1;
         ev[q * W + j] = j < len ? v[k0 + j] : 0.0;
     }
+    if (erow) erow[q] = q < n ? (ord ? ord[q] : static_cast<int>(q)) : -1;
 }
 
 // ------------------------------------------------------------ helpers ------
@@ -741,9 +744,10 @@ Status permute_rows(decmg_gpu_ctx* c, int nrows, const int* ord, const int* rp, 
     return Status::Ok();
 }
 
-// Padded ELL copy of a row-ordered CSR when every row has <= W entries.
-Status build_ell(decmg_gpu_ctx* c, int nrows, const int* rp, const int* ci, const double* v, int W, int** eci,
-                 double** ev) {
+// Padded ELL copy of a row-ordered CSR when every row has <= W entries;
+// rows padded to a multiple of 224 (the largest pipelined tile, cycle.cu).
+Status build_ell(decmg_gpu_ctx* c, int nrows, const int* rp, const int* ci, const double* v, const int* ord, int W,
+                 int** eci, double** ev, int** erow) {
     TmpPool tp(c->stream);
     int* mx;
     DG_TRY(tp.get(&mx, 1));
@@ -756,9 +760,11 @@ Status build_ell(decmg_gpu_ctx* c, int nrows, const int* rp, const int* ci, cons
         *ev = nullptr;
         return Status::Ok();
     }
-    DG_TRY(dalloc(c, eci, static_cast<size_t>(nrows) * W));
-    DG_TRY(dalloc(c, ev, static_cast<size_t>(nrows) * W));
-    LAUNCH(4, nrows, k_ell_fill, nrows, W, rp, ci, v, *eci, *ev);
+    const int npad = (nrows + 223) / 224 * 224;
+    DG_TRY(dalloc(c, eci, static_cast<size_t>(npad) * W));
+    DG_TRY(dalloc(c, ev, static_cast<size_t>(npad) * W));
+    if (erow) DG_TRY(dalloc(c, erow, npad));
+    LAUNCH(4, npad, k_ell_fill, nrows, npad, W, rp, ci, v, ord, *eci, *ev, erow ? *erow : nullptr);
     return Status::Ok();
 }
 
@@ -792,9 +798,13 @@ Status build_orders(decmg_gpu_ctx* c) {
     for (int k = 0; k + 1 < L; ++k) {  // the coarsest level only runs the sequential CG
         Level& m = c->lv[k];
         const Level& cm = c->lv[k + 1];
-        DG_TRY(build_ell(c, m.nv, m.Lo_rp, m.Lo_ci, m.Lo_v, 8, &m.Le_ci, &m.Le_v));
-        DG_TRY(build_ell(c, m.nv, m.Po_rp, m.Po_ci, m.Po_v, 2, &m.Pe_ci, &m.Pe_v));
-        DG_TRY(build_ell(c, cm.nv, m.Ro_rp, m.Ro_ci, m.Ro_v, 8, &m.Re_ci, &m.Re_v));
+        DG_TRY(build_ell(c, m.nv, m.Lo_rp, m.Lo_ci, m.Lo_v, m.ord, 8, &m.Le_ci, &m.Le_v, &m.Le_row));
+        DG_TRY(build_ell(c, m.nv, m.Po_rp, m.Po_ci, m.Po_v, m.ord, 2, &m.Pe_ci, &m.Pe_v, nullptr));
+        DG_TRY(build_ell(c, cm.nv, m.Ro_rp, m.Ro_ci, m.Ro_v, cm.ord, 8, &m.Re_ci, &m.Re_v, &m.Re_row));
+        if (m.Pe_ci && !m.Le_row) {  // P rows share L's row ids
+            m.Pe_ci = nullptr;
+            m.Pe_v = nullptr;
+        }
     }
     DG_CUDA(cudaStreamSynchronize(c->stream));
     return Status::Ok();
