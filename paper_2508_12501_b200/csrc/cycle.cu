@@ -442,13 +442,17 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_rowop_pipe(PipeArgs a) {
         }
     }
     if constexpr (OP == OP_RES_NORM) {
-        // fold the consumers' accumulators: [ROWS][BP] in a fixed tree order
-        __shared__ double sh[kPipeConsumers * RPT];
+        // fold the consumers' accumulators: [ROWS][BP] in a fixed tree order,
+        // rows padded with zeros to a power of two (ROWS = 224 / TPR is not one)
+        constexpr int RP2 = ROWS <= 1 ? 1 : (ROWS <= 2 ? 2 : (ROWS <= 4 ? 4 : (ROWS <= 8 ? 8 : (ROWS <= 16 ? 16 :
+                            (ROWS <= 32 ? 32 : (ROWS <= 64 ? 64 : (ROWS <= 128 ? 128 : 256)))))));
+        __shared__ double sh[RP2 * BP];
+        for (int idx = kPipeConsumers * RPT + tid; idx < RP2 * BP; idx += kPipeThreads) sh[idx] = 0.0;
         if (tid < kPipeConsumers)
 #pragma unroll
             for (int l = 0; l < RPT; ++l) sh[tid * RPT + l] = acc[l];
         __syncthreads();
-        for (int sft = ROWS / 2; sft >= 1; sft >>= 1) {
+        for (int sft = RP2 / 2; sft >= 1; sft >>= 1) {
             for (int idx = tid; idx < sft * BP; idx += kPipeThreads) sh[idx] = __dadd_rn(sh[idx], sh[idx + sft * BP]);
             __syncthreads();
         }
