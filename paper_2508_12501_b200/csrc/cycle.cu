@@ -349,7 +349,12 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_rowop_pipe(PipeArgs a) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    // contiguous tile ranges per CTA: spatially adjacent rows (Morton order)
+    // stay on one SM, so the x lines they share are reused from L1
     const int ntiles = a.ntiles;
+    const int per = (ntiles + gridDim.x - 1) / gridDim.x;
+    const int t_begin = blockIdx.x * per;
+    const int t_end = t_begin + per < ntiles ? t_begin + per : ntiles;
     double acc[RPT];
 #pragma unroll
     for (int l = 0; l < RPT; ++l) acc[l] = 0.0;
@@ -357,7 +362,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_rowop_pipe(PipeArgs a) {
     if (tid >= kPipeConsumers) {
         if (tid == kPipeConsumers) {  // producer
             int i = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            for (int t = t_begin; t < t_end; ++t, ++i) {
                 const int s = i % kPipeStages;
                 if (i >= kPipeStages) mbar_wait(&empty[s], ((i / kPipeStages) - 1) & 1);
                 unsigned char* st = smem_raw + static_cast<size_t>(s) * G::STAGE_BYTES;
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_rowop_pipe(PipeArgs a) {
         const int lane0 = (tid % TPR) * RPT;
         const int nrhs = a.nrhs;
         int i = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        for (int t = t_begin; t < t_end; ++t, ++i) {
             const int s = i % kPipeStages;
             mbar_wait(&full[s], (i / kPipeStages) & 1);
             const unsigned char* st = smem_raw + static_cast<size_t>(s) * G::STAGE_BYTES;
@@ -557,11 +562,19 @@ __global__ void __launch_bounds__(64) k_project_sums(int n, int nrhs, const doub
             const double* bt = bbuf + static_cast<size_t>(s) * kProjRows * nrhs;
             const double* wt = wbuf + s * kProjRows;
             if (lane < nrhs) {
-#pragma unroll 8
-                for (int i = 0; i < kProjRows; ++i) {
-                    const double wv = wt[i];
-                    mean = __dadd_rn(mean, __dmul_rn(wv, bt[i * nrhs + lane]));
-                    total = __dadd_rn(total, wv);
+                // products first (independent), then the dependent add chains
+                for (int i0 = 0; i0 < kProjRows; i0 += 16) {
+                    double p[16], wv[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        wv[u] = wt[i0 + u];
+                        p[u] = __dmul_rn(wv[u], bt[(i0 + u) * nrhs + lane]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        mean = __dadd_rn(mean, p[u]);
+                        total = __dadd_rn(total, wv[u]);
+                    }
                 }
             }
             __syncwarp();
