@@ -24,7 +24,6 @@ import json
 import os
 import subprocess
 import sys
-import threading
 import time
 from pathlib import Path
 
@@ -81,7 +80,8 @@ def sum_over_ranks(world, v: float) -> float:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms while the
+    timed region runs (`nvidia-smi -lms 50` in the background)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -89,43 +89,43 @@ class ClockSampler:
 
     def __init__(self, device: int):
         self.device = device
-        self.samples = []
-        self._stop = threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self.proc = None
+        self.out = ""
 
     def __enter__(self):
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.15)  # first sample before the timed work starts
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self.proc is not None:
+            time.sleep(0.06)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                self.out = ""
 
     def summary(self):
-        if not self.samples:
+        samples = [[x.strip() for x in ln.split(",")] for ln in self.out.splitlines() if ln.count(",") >= 6]
+        if not samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        sm = [float(s[0]) for s in samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for s in self.samples:
-            for name, v in zip(names, s[3:7]):
+        for smp in samples:
+            for name, v in zip(names, smp[3:7]):
                 if v.strip().lower() == "active":
                     reasons.add(name)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+                "reasons": sorted(reasons), "samples": len(samples)}
 
 
 def measured_peak():
@@ -206,7 +206,7 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     # timed: exactly K steps, one run_cycle call of K cycles from zero
     h.set_timing(True)
-    h.timing(7)  # reset per-class accumulators
+    h.timing(-1)  # reset per-class accumulators
     launches0 = h.launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -220,7 +220,7 @@ def run_ours(args, world, rank, local):
         barrier(world)
     ms = ev0.elapsed_time(ev1)
     launches = h.launch_count() - launches0
-    cls = {c: h.timing(c) for c in range(7)}
+    cls = {c: h.timing(c) for c in range(8)}
     h.set_timing(False)
     hist = d_hist[: args.steps].cpu().numpy()
     ms_max = max_over_ranks(world, ms)
@@ -235,14 +235,14 @@ def run_ours(args, world, rank, local):
     bytes_per_launch = tbytes / max(nl, 1)
     achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9 if nl else None
     kern_total = sum(v[1] for v in cls.values())
-    roofline = {"bound": "hbm", "kernel": "k_sweep<16> (fine-level weighted-Jacobi sweep, level 0)",
+    roofline = {"bound": "hbm", "kernel": "k_rowop_pipe<16,4,8,OP_SWEEP> (level-0 weighted-Jacobi sweep)",
                 "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None, "traffic": ncu_traffic(),
                 "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
                 "launches": nl, "share_of_kernel_time": tms / kern_total if kern_total else None,
                 "classes_ms": {k: round(v[1], 4) for k, v in zip(
                     ["fine_sweep", "fine_residual", "restrict", "prolong", "coarse_levels", "coarse_solve",
-                     "norms"], cls.values())}}
+                     "norms", "zero_start_sweeps"], cls.values())}}
 
     # e2e: public host-pointer API, pinned host buffers, full gmg_solve to 1e-8
     # per step (H2D of the 16 right-hand sides, D2H of the 16 solutions).

@@ -147,8 +147,10 @@ DECMG_API int64_t decmg_gpu_export(decmg_gpu_ctx* ctx, int level, const char* na
 DECMG_API int decmg_gpu_mesh_hash(decmg_gpu_ctx* ctx, int level, uint64_t* hash);
 
 /* Per-kernel device timing (CUDA events around every launch when enabled).
- * Kernel classes: 0 fine sweep, 1 fine residual, 2 restrict, 3 prolong,
- * 4 coarse-level work, 5 coarse solve, 6 norms. */
+ * Kernel classes: 0 level-0 sweep, 1 level-0 residual, 2 level-0 restrict,
+ * 3 level-0 prolong, 4 coarser-level work, 5 coarse solve, 6 norms and
+ * projections, 7 zero-start sweeps. cls = -1 resets the accumulators.
+ * bytes = algorithmic bytes of the launches. */
 DECMG_API int decmg_gpu_set_timing(decmg_gpu_ctx* ctx, int enable);
 DECMG_API int decmg_gpu_get_timing(decmg_gpu_ctx* ctx, int cls, int64_t* launches, double* total_ms,
                          double* bytes);

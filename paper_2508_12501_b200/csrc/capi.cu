@@ -325,7 +325,7 @@ int decmg_gpu_set_timing(decmg_gpu_ctx* ctx, int enable) {
 }
 
 int decmg_gpu_get_timing(decmg_gpu_ctx* ctx, int cls, int64_t* launches, double* total_ms, double* bytes) {
-    if (!ctx || cls < 0 || cls >= 8) return DECMG_INVALID_ARGUMENT;
+    if (!ctx || cls < -1 || cls >= 8) return DECMG_INVALID_ARGUMENT;
     cudaSetDevice(ctx->device);
     auto& T = ctx->timing;
     if (!T.recs.empty()) {
@@ -341,16 +341,17 @@ int decmg_gpu_get_timing(decmg_gpu_ctx* ctx, int cls, int64_t* launches, double*
         }
         T.recs.clear();
     }
-    if (launches) *launches = T.launches[cls];
-    if (total_ms) *total_ms = T.ms[cls];
-    if (bytes) *bytes = T.bytes[cls];
-    if (cls == 7) {  // class 7 read resets all accumulators
+    if (cls == -1) {  // reset all accumulators
         for (int i = 0; i < 8; ++i) {
             T.launches[i] = 0;
             T.ms[i] = 0;
             T.bytes[i] = 0;
         }
+        return DECMG_OK;
     }
+    if (launches) *launches = T.launches[cls];
+    if (total_ms) *total_ms = T.ms[cls];
+    if (bytes) *bytes = T.bytes[cls];
     return DECMG_OK;
 }
 

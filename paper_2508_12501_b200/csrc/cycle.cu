@@ -707,7 +707,7 @@ inline int bp_of(int nrhs) {
     }
 
 enum Cls { kFineSweep = 0, kFineResidual = 1, kRestrict = 2, kProlong = 3, kCoarseLevels = 4,
-           kCoarseSolve = 5, kNorms = 6 };
+           kCoarseSolve = 5, kNorms = 6, kZeroSweep = 7 };
 
 struct Driver {
     decmg_gpu_ctx* c;
@@ -775,7 +775,7 @@ struct Driver {
             const double* b = bptr(k);
             if (L.x_zero) {
                 const double bytes = 8.0 * L.nv + 16.0 * L.nv * R;
-                DG_TRY(launch(c, k == 0 ? kFineSweep : kCoarseLevels, bytes, [&] {
+                DG_TRY(launch(c, kZeroSweep, bytes, [&] {
                     DISPATCH_BP(key, k_sweep_zero<BP, RPT><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
                                         L.nv, nrhs, L.diag, b, xo, plan.omega));
                 }));
