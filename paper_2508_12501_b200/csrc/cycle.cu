@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <functional>
 
 namespace decmg_gpu {
 namespace {
@@ -304,13 +305,16 @@ __global__ void __launch_bounds__(kBlock, 2) k_prolong_add(int n, int nrhs, cons
 // including the residual-norm partials, is deterministic for a given grid.
 //
 // OP: 0 sweep (jacobi_sweep), 1 residual store, 2 residual norm partials,
-//     3 y = A x with Dirichlet zero rows (restriction), 4 x += P xc (prolong).
+//     3 y = A x with Dirichlet zero rows (restriction), 4 x += P xc (prolong),
+//     5 sweep that also emits the norm partials of b - A x for the incoming x
+//       (the previous cycle's fine residual; same arithmetic and tile/CTA
+//       partition as op 2, so the norm is bit-identical to a separate pass).
 // 7 consumer warps + 1 producer warp: two CTAs per SM put 4 warps on each
 // SM sub-partition, which leaves 128 registers per thread.
 constexpr int kPipeConsumers = 224;
 constexpr int kPipeThreads = kPipeConsumers + 32;
 constexpr int kPipeStages = 4;
-enum { OP_SWEEP = 0, OP_RES_STORE = 1, OP_RES_NORM = 2, OP_SPMV = 3, OP_PROLONG = 4 };
+enum { OP_SWEEP = 0, OP_RES_STORE = 1, OP_RES_NORM = 2, OP_SPMV = 3, OP_PROLONG = 4, OP_SWEEP_NORM = 5 };
 
 struct PipeArgs {
     int ntiles, nrhs;
@@ -395,7 +399,8 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_rowop_pipe(PipeArgs a) {
             const int64_t o = row * nrhs + lane0;
             double pre[RPT], xv[W][RPT], sum[RPT], xr[RPT], d = 0.0;
             if (active) {
-                if constexpr (OP == OP_SWEEP || OP == OP_RES_STORE || OP == OP_RES_NORM) ldv<RPT>(a.b + o, pre);
+                if constexpr (OP == OP_SWEEP || OP == OP_SWEEP_NORM || OP == OP_RES_STORE || OP == OP_RES_NORM)
+                    ldv<RPT>(a.b + o, pre);
                 if constexpr (OP == OP_PROLONG) ldv<RPT>(a.out + o, pre);
 #pragma unroll
                 for (int j = 0; j < W; ++j) {
@@ -411,11 +416,11 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_rowop_pipe(PipeArgs a) {
                         const double vj = vq[j];
 #pragma unroll
                         for (int l = 0; l < RPT; ++l) sum[l] = __dadd_rn(sum[l], __dmul_rn(vj, xv[j][l]));
-                        if (OP == OP_SWEEP && cj == row32) d = vj;
+                        if ((OP == OP_SWEEP || OP == OP_SWEEP_NORM) && cj == row32) d = vj;
                     }
                 }
                 // x_ii: re-read (an L1 hit -- the diagonal gather just brought it in)
-                if constexpr (OP == OP_SWEEP) ldv<RPT>(a.x + o, xr);
+                if constexpr (OP == OP_SWEEP || OP == OP_SWEEP_NORM) ldv<RPT>(a.x + o, xr);
             }
             __syncwarp();
             if ((tid & 31) == 0) mbar_arrive(&empty[s]);  // stage consumed
@@ -423,7 +428,11 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_rowop_pipe(PipeArgs a) {
             double res[RPT];
 #pragma unroll
             for (int l = 0; l < RPT; ++l) {
-                if constexpr (OP == OP_SWEEP)
+                if constexpr (OP == OP_SWEEP_NORM) {
+                    const double rl = __dsub_rn(pre[l], sum[l]);
+                    acc[l] = __dadd_rn(acc[l], __dmul_rn(rl, rl));
+                }
+                if constexpr (OP == OP_SWEEP || OP == OP_SWEEP_NORM)
                     res[l] = __dadd_rn(xr[l], __ddiv_rn(__dmul_rn(a.omega, __dsub_rn(pre[l], sum[l])), d));
                 else if constexpr (OP == OP_RES_STORE || OP == OP_RES_NORM)
                     res[l] = __dsub_rn(pre[l], sum[l]);
@@ -446,7 +455,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_rowop_pipe(PipeArgs a) {
             }
         }
     }
-    if constexpr (OP == OP_RES_NORM) {
+    if constexpr (OP == OP_RES_NORM || OP == OP_SWEEP_NORM) {
         // fold the consumers' accumulators: [ROWS][BP] in a fixed tree order,
         // rows padded with zeros to a power of two (ROWS = 224 / TPR is not one)
         constexpr int RP2 = ROWS <= 1 ? 1 : (ROWS <= 2 ? 2 : (ROWS <= 4 ? 4 : (ROWS <= 8 ? 8 : (ROWS <= 16 ? 16 :
@@ -713,8 +722,16 @@ struct Driver {
     decmg_gpu_ctx* c;
     int nrhs, bp;
     const double* b0;  // level-0 right-hand side
-    int key = 0;       // DISPATCH_BP key of the row kernels (-bp: vector mapping)
+    int key = 0;       // DISPATCH_BP key of the row kernels (10 * BP + RPT)
     int tpr = 1;       // threads per row
+    // Fused residual norm: when set, the next level-0 sweep also writes
+    // ||b - A x|| / denom of the x it reads into fuse_hist, then calls
+    // fuse_hook(xprev, &stop); stop == true undoes the sweep's buffer flip and
+    // abandons the rest of the cycle (gmg_solve's convergence exit).
+    double* fuse_hist = nullptr;
+    const double* fuse_denom = nullptr;
+    std::function<Status(const double*, bool*)> fuse_hook;
+    bool stopped = false;
 
     void init() {
         const bool vec = nrhs == bp && bp >= 2;
@@ -782,7 +799,25 @@ struct Driver {
             } else {
                 const double bytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
                 const double* x = xcur(L);
-                if (L.Le_ci && tpr <= 8) {
+                if (k == 0 && it == 0 && fuse_hist && L.Le_ci && tpr <= 8) {
+                    int g = 0;
+                    DG_TRY((pipe<OP_SWEEP_NORM, 8>(kFineSweep, bytes, L.nv, L.Le_ci, L.Le_v, L.Le_row, x, b, xo,
+                                                   c->red, nullptr, plan.omega, &g)));
+                    DG_TRY(reduce_partials(g, fuse_hist, 2, fuse_denom));
+                    fuse_hist = nullptr;
+                    L.cur ^= 1;
+                    L.x_zero = false;
+                    if (fuse_hook) {
+                        bool stop = false;
+                        DG_TRY(fuse_hook(L.x[L.cur ^ 1], &stop));
+                        if (stop) {
+                            L.cur ^= 1;  // x_prev stays the current iterate
+                            stopped = true;
+                            return Status::Ok();
+                        }
+                    }
+                    continue;
+                } else if (L.Le_ci && tpr <= 8) {
                     DG_TRY((pipe<OP_SWEEP, 8>(k == 0 ? kFineSweep : kCoarseLevels, bytes, L.nv, L.Le_ci, L.Le_v,
                                               L.Le_row, x, b, xo, nullptr, nullptr, plan.omega)));
                 } else {
@@ -873,6 +908,7 @@ struct Driver {
         for (int w = 0; w < nw; ++w) {
             if (plan.walk[w] == 'd') {
                 DG_TRY(smooth(level, plan.pre[level], plan));
+                if (stopped) return Status::Ok();
                 DG_TRY(residual_restrict(level));
                 ++level;
                 c->lv[level].x_zero = true;  // kernels::fill(0.0, xs[level])
@@ -943,6 +979,15 @@ struct Driver {
         DG_TRY(sumsq(b0, bn, 1));
         DG_TRY(launch(c, kNorms, 0.0, [&] { k_denom<<<1, 32, 0, c->stream>>>(nrhs, bn, denom); }));
         return Status::Ok();
+    }
+
+    // Can the next cycle's first level-0 sweep carry the residual norm of the
+    // current iterate? (walk starts with a level-0 pre-smoothing on the
+    // pipelined path and x is materialized)
+    bool can_fuse(const Plan& plan) const {
+        const Level& L = c->lv[0];
+        return c->lv.size() > 1 && !plan.walk.empty() && plan.walk[0] == 'd' && plan.pre[0] >= 1 && !L.x_zero &&
+               L.Le_ci && tpr <= 8 && L.zero_diag_row < 0;
     }
 
     Status one_cycle(const Plan& plan) {
@@ -1016,9 +1061,17 @@ Status run_cycles(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_
     double* denom = c->dsmall;
     DG_TRY(dr.load_x0(d_x0));
     DG_TRY(dr.make_denom(denom));
+    // hist[c] = residual of the iterate after cycle c: computed by the first
+    // level-0 sweep of cycle c+1 when possible, else by a separate pass.
     for (int cyc = 0; cyc < ncycles; ++cyc) {
         DG_TRY(dr.one_cycle(plan));
-        DG_TRY(dr.resnorm(d_hist + static_cast<int64_t>(cyc) * nrhs, denom));
+        double* hc = d_hist + static_cast<int64_t>(cyc) * nrhs;
+        if (cyc + 1 < ncycles && dr.can_fuse(plan)) {
+            dr.fuse_hist = hc;
+            dr.fuse_denom = denom;
+        } else {
+            DG_TRY(dr.resnorm(hc, denom));
+        }
     }
     DG_TRY(dr.ensure_x(0));
     Level& L = c->lv[0];
@@ -1075,12 +1128,11 @@ Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, co
         DG_CUDA(cudaStreamSynchronize(c->stream));
         for (int l = 0; l < nrhs; ++l) final_res[l] = c->hsmall[l];
     }
-    while (cyc < max_cycles && active) {
-        DG_TRY(dr.one_cycle(plan));
-        DG_TRY(dr.resnorm(dres, denom));
+    // Record the residual of the iterate after `cyc` cycles (in dres) and
+    // retire the right-hand sides that reached tol; xsrc holds that iterate.
+    auto check = [&](const double* xsrc) -> Status {
         DG_CUDA(cudaMemcpyAsync(c->hsmall, dres, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, c->stream));
         DG_CUDA(cudaStreamSynchronize(c->stream));
-        ++cyc;
         unsigned fin = 0;
         for (int l = 0; l < nrhs; ++l) {
             if (!(active & (1u << l))) continue;
@@ -1091,13 +1143,42 @@ Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, co
             if (res <= tol || cyc == max_cycles) fin |= 1u << l;
         }
         if (fin) {
-            DG_TRY(dr.ensure_x(0));
-            const double* src = L0.x[L0.cur];
             DG_TRY(launch(c, kNorms, 16.0 * L0.nv * nrhs, [&] {
-                k_copy_lanes<<<grid_for(total, kBlock), kBlock, 0, c->stream>>>(total, nrhs, fin, src, c->xsol);
+                k_copy_lanes<<<grid_for(total, kBlock), kBlock, 0, c->stream>>>(total, nrhs, fin, xsrc, c->xsol);
             }));
             active &= ~fin;
         }
+        return Status::Ok();
+    };
+    while (cyc < max_cycles && active) {
+        if (cyc > 0 && dr.can_fuse(plan)) {
+            // the first level-0 sweep of the next cycle yields the residual of
+            // the current iterate; stop there if every RHS has converged
+            dr.fuse_hist = dres;
+            dr.fuse_denom = denom;
+            dr.fuse_hook = [&](const double* xprev, bool* stop) -> Status {
+                DG_TRY(check(xprev));
+                *stop = active == 0;
+                return Status::Ok();
+            };
+            dr.stopped = false;
+            DG_TRY(dr.one_cycle(plan));
+            dr.fuse_hook = nullptr;
+            if (dr.stopped) break;
+        } else {
+            if (cyc > 0) {
+                DG_TRY(dr.resnorm(dres, denom));
+                DG_TRY(check(L0.x[L0.cur]));
+                if (!active) break;
+            }
+            DG_TRY(dr.one_cycle(plan));
+        }
+        ++cyc;
+    }
+    if (active && cyc > 0) {  // residual of the last iterate (cycle cap or last cycle)
+        DG_TRY(dr.ensure_x(0));
+        DG_TRY(dr.resnorm(dres, denom));
+        DG_TRY(check(L0.x[L0.cur]));
     }
     if (active) {  // max_cycles == 0: the solution is x0
         DG_TRY(dr.ensure_x(0));
