@@ -91,6 +91,8 @@ struct Level {
     double* Pe_v = nullptr;
     int* Re_ci = nullptr;
     double* Re_v = nullptr;
+    int Le_w = 0;            // ELL widths (7 or 8; 0 = no ELL copy)
+    int Re_w = 0;
     int* Le_row = nullptr;   // original row id per ELL row of Le/Pe (padded, -1 = padding)
     int* Re_row = nullptr;   // original coarse row id per ELL row of Re
     int zero_diag_row = -1;  // first row with L_ii == 0 (-1: none)

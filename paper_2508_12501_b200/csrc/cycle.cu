@@ -718,6 +718,9 @@ inline int bp_of(int nrhs) {
 enum Cls { kFineSweep = 0, kFineResidual = 1, kRestrict = 2, kProlong = 3, kCoarseLevels = 4,
            kCoarseSolve = 5, kNorms = 6, kZeroSweep = 7 };
 
+// Dispatch the pipelined kernel on the ELL width of an operator (7 or 8).
+#define PIPE_W(w, OP, ...) ((w) == 7 ? pipe<OP, 7>(__VA_ARGS__) : pipe<OP, 8>(__VA_ARGS__))
+
 struct Driver {
     decmg_gpu_ctx* c;
     int nrhs, bp;
@@ -754,7 +757,7 @@ struct Driver {
         Status st;
         DISPATCH_BP(key, {
             using G = PipeGeom<BP, RPT, W>;
-            static_assert(G::ROWS * 4 % 16 == 0 || BP / RPT > 8, "pipe tile");
+            static_assert((G::ROWS * 4 % 16 == 0 && G::CI_BYTES % 16 == 0) || BP / RPT > 8, "pipe tile");
             const int ntiles = (nrows + G::ROWS - 1) / G::ROWS;
             const int g = ntiles < 2 * c->num_sms ? ntiles : 2 * c->num_sms;
             static bool attr = false;
@@ -801,8 +804,8 @@ struct Driver {
                 const double* x = xcur(L);
                 if (k == 0 && it == 0 && fuse_hist && L.Le_ci && tpr <= 8) {
                     int g = 0;
-                    DG_TRY((pipe<OP_SWEEP_NORM, 8>(kFineSweep, bytes, L.nv, L.Le_ci, L.Le_v, L.Le_row, x, b, xo,
-                                                   c->red, nullptr, plan.omega, &g)));
+                    DG_TRY(PIPE_W(L.Le_w, OP_SWEEP_NORM, kFineSweep, bytes, L.nv, L.Le_ci, L.Le_v, L.Le_row, x, b,
+                                  xo, c->red, nullptr, plan.omega, &g));
                     DG_TRY(reduce_partials(g, fuse_hist, 2, fuse_denom));
                     fuse_hist = nullptr;
                     L.cur ^= 1;
@@ -818,8 +821,8 @@ struct Driver {
                     }
                     continue;
                 } else if (L.Le_ci && tpr <= 8) {
-                    DG_TRY((pipe<OP_SWEEP, 8>(k == 0 ? kFineSweep : kCoarseLevels, bytes, L.nv, L.Le_ci, L.Le_v,
-                                              L.Le_row, x, b, xo, nullptr, nullptr, plan.omega)));
+                    DG_TRY(PIPE_W(L.Le_w, OP_SWEEP, k == 0 ? kFineSweep : kCoarseLevels, bytes, L.nv, L.Le_ci,
+                                  L.Le_v, L.Le_row, x, b, xo, nullptr, nullptr, plan.omega, nullptr));
                 } else {
                     DG_TRY(launch(c, k == 0 ? kFineSweep : kCoarseLevels, bytes, [&] {
                         DISPATCH_BP(key, (k_sweep<BP, RPT, 0><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
@@ -843,8 +846,8 @@ struct Driver {
         const double* b = bptr(k);
         const double rbytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
         if (L.Le_ci && tpr <= 8) {
-            DG_TRY((pipe<OP_RES_STORE, 8>(k == 0 ? kFineResidual : kCoarseLevels, rbytes, L.nv, L.Le_ci, L.Le_v,
-                                          L.Le_row, x, b, c->r, nullptr, nullptr, 0.0)));
+            DG_TRY(PIPE_W(L.Le_w, OP_RES_STORE, k == 0 ? kFineResidual : kCoarseLevels, rbytes, L.nv, L.Le_ci,
+                          L.Le_v, L.Le_row, x, b, c->r, nullptr, nullptr, 0.0, nullptr));
         } else {
             DG_TRY(launch(c, k == 0 ? kFineResidual : kCoarseLevels, rbytes, [&] {
                 DISPATCH_BP(key, (k_residual<BP, RPT, 0, true><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
@@ -854,8 +857,8 @@ struct Driver {
         const double tbytes = 12.0 * L.nnzR + 4.0 * (C.nv + 1) + 8.0 * L.nv * R + 8.0 * C.nv * R;
         const int* zr = c->dirichlet ? C.bd : nullptr;
         if (L.Re_ci && tpr <= 8) {
-            DG_TRY((pipe<OP_SPMV, 8>(k == 0 ? kRestrict : kCoarseLevels, tbytes, C.nv, L.Re_ci, L.Re_v, L.Re_row,
-                                     c->r, nullptr, C.b, nullptr, zr, 0.0)));
+            DG_TRY(PIPE_W(L.Re_w, OP_SPMV, k == 0 ? kRestrict : kCoarseLevels, tbytes, C.nv, L.Re_ci, L.Re_v,
+                          L.Re_row, c->r, nullptr, C.b, nullptr, zr, 0.0, nullptr));
         } else {
             DG_TRY(launch(c, k == 0 ? kRestrict : kCoarseLevels, tbytes, [&] {
                 DISPATCH_BP(key, (k_spmv<BP, RPT, 0><<<rows_grid(C.nv), kBlock, 0, c->stream>>>(
@@ -962,8 +965,8 @@ struct Driver {
         const double bytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 16.0 * L.nv * nrhs;
         if (L.Le_ci && tpr <= 8) {
             int g = 0;
-            DG_TRY((pipe<OP_RES_NORM, 8>(kFineResidual, bytes, L.nv, L.Le_ci, L.Le_v, L.Le_row, x, b0, nullptr,
-                                         c->red, nullptr, 0.0, &g)));
+            DG_TRY(PIPE_W(L.Le_w, OP_RES_NORM, kFineResidual, bytes, L.nv, L.Le_ci, L.Le_v, L.Le_row, x, b0,
+                          nullptr, c->red, nullptr, 0.0, &g));
             return reduce_partials(g, hist, 2, denom);
         }
         DG_TRY(launch(c, kFineResidual, bytes, [&] {

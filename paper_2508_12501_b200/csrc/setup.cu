@@ -746,8 +746,9 @@ Status permute_rows(decmg_gpu_ctx* c, int nrows, const int* ord, const int* rp, 
 
 // Padded ELL copy of a row-ordered CSR when every row has <= W entries;
 // rows padded to a multiple of 224 (the largest pipelined tile, cycle.cu).
+// W < 0: pick the narrowest of |W|-1 and |W| that fits (7 or 8); *wout = width used.
 Status build_ell(decmg_gpu_ctx* c, int nrows, const int* rp, const int* ci, const double* v, const int* ord, int W,
-                 int** eci, double** ev, int** erow) {
+                 int** eci, double** ev, int** erow, int* wout = nullptr) {
     TmpPool tp(c->stream);
     int* mx;
     DG_TRY(tp.get(&mx, 1));
@@ -755,6 +756,8 @@ Status build_ell(decmg_gpu_ctx* c, int nrows, const int* rp, const int* ci, cons
     LAUNCH(4, nrows, k_row_maxlen, nrows, rp, mx);
     int h = 0;
     DG_TRY(read_int(c, mx, &h));
+    if (W < 0) W = h <= -W - 1 ? -W - 1 : -W;
+    if (wout) *wout = h > W ? 0 : W;
     if (h > W) {
         *eci = nullptr;
         *ev = nullptr;
@@ -798,9 +801,9 @@ Status build_orders(decmg_gpu_ctx* c) {
     for (int k = 0; k + 1 < L; ++k) {  // the coarsest level only runs the sequential CG
         Level& m = c->lv[k];
         const Level& cm = c->lv[k + 1];
-        DG_TRY(build_ell(c, m.nv, m.Lo_rp, m.Lo_ci, m.Lo_v, m.ord, 8, &m.Le_ci, &m.Le_v, &m.Le_row));
+        DG_TRY(build_ell(c, m.nv, m.Lo_rp, m.Lo_ci, m.Lo_v, m.ord, -8, &m.Le_ci, &m.Le_v, &m.Le_row, &m.Le_w));
         DG_TRY(build_ell(c, m.nv, m.Po_rp, m.Po_ci, m.Po_v, m.ord, 2, &m.Pe_ci, &m.Pe_v, nullptr));
-        DG_TRY(build_ell(c, cm.nv, m.Ro_rp, m.Ro_ci, m.Ro_v, cm.ord, 8, &m.Re_ci, &m.Re_v, &m.Re_row));
+        DG_TRY(build_ell(c, cm.nv, m.Ro_rp, m.Ro_ci, m.Ro_v, cm.ord, -8, &m.Re_ci, &m.Re_v, &m.Re_row, &m.Re_w));
         if (m.Pe_ci && !m.Le_row) {  // P rows share L's row ids
             m.Pe_ci = nullptr;
             m.Pe_v = nullptr;
