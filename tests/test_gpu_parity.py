@@ -277,3 +277,33 @@ def test_config4_full_size(nsub):
     np.testing.assert_array_equal(res.x[:, 0], ox)
     assert np.all(np.abs(res.residual_history[:, 0] - oh) <= RTOL_HIST * oh)
     assert np.all(res.residual_history[1] < 0.5 * res.residual_history[0])
+
+
+@pytest.mark.parametrize("base,nsub,dirichlet,rhs", [("square", 12, True, "uniform"), ("ico", 11, False, "uniform")])
+def test_config5_full_size(base, nsub, dirichlet, rhs):
+    """BASELINE config 5 single-GPU (5a: unit square x12, 16,785,409 vertices,
+    Dirichlet; 5b: icosphere x11, 41,943,042 vertices): finest-mesh hash and
+    L values against the oracle, bit-identical iterate after two V(2,2)
+    cycles, and a full gmg_solve to 1e-8 with the per-cycle history matching
+    the oracle's first cycles."""
+    h = d.MultigridHierarchy.from_base(base, nsub, dirichlet=dirichlet)
+    n = h.n()
+    assert n == ((2 ** nsub + 1) ** 2 if base == "square" else 10 * 4 ** nsub + 2)
+    o = OracleHierarchy(base, nsub, dirichlet)
+    assert h.mesh_hash(0) == o.info(0)["hash"]
+    assert fnv(h.export(0, "L_values")) == fnv(o.get(0, "L_v"))
+    b = h.make_rhs(rhs, 7)
+    ob = o.rhs(rhs, 7)
+    np.testing.assert_array_equal(b, ob)
+    bp = ob if dirichlet else o.project(ob)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan.cycles = 2
+    res = h.run_cycle(plan, bp)
+    ox, oh = o.run_cycles(bp, ncycles=2)
+    np.testing.assert_array_equal(res.x, ox)
+    assert np.all(np.abs(res.residual_history - oh) <= RTOL_HIST * oh)
+    rep = d.gmg_solve(h, d.standard_plan(h.levels(), d.CycleKind.V, 2, 2), b, 1e-8, 200)
+    assert rep.converged and rep.final_relative_residual <= 1e-8
+    hist = np.array(rep.residual_history)
+    assert np.all(hist[1:] < hist[:-1])
+    np.testing.assert_allclose(hist[:2], oh, rtol=RTOL_HIST)
