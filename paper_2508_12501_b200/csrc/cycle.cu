@@ -19,8 +19,7 @@
 // so sweeps, residuals and transfers are bit-identical to the reference.
 // Norms and projections use a fixed-shape tree reduction: deterministic run
 // to run, within a few ulps of the reference's blocked sums.
-#include "common.cuh"
-#include "ptx.cuh"
+#include "rowkernels.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -28,695 +27,6 @@
 
 namespace decmg_gpu {
 namespace {
-
-constexpr int kBlock = 256;
-
-__device__ __forceinline__ int64_t gtid() {
-    return static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-}
-
-// Thread mapping. A row is owned by TPR = BP / RPT consecutive threads and
-// each thread owns RPT consecutive right-hand sides (lanes sub*RPT ..
-// sub*RPT + RPT - 1), loaded with 16-byte vector accesses. RPT > 1 only when
-// nrhs == BP (full, 16-byte aligned rows). Per-lane arithmetic is unchanged,
-// so the mapping never affects the bits of a result.
-template <int RPT>
-__device__ __forceinline__ void ldv(const double* __restrict__ p, double (&o)[RPT]) {
-    if constexpr (RPT == 1) {
-        o[0] = *p;
-    } else {
-#pragma unroll
-        for (int j = 0; j < RPT / 2; ++j) {
-            const double2 t = *reinterpret_cast<const double2*>(p + 2 * j);
-            o[2 * j] = t.x;
-            o[2 * j + 1] = t.y;
-        }
-    }
-}
-template <int RPT>
-__device__ __forceinline__ void stv(double* __restrict__ p, const double (&o)[RPT]) {
-    if constexpr (RPT == 1) {
-        *p = o[0];
-    } else {
-#pragma unroll
-        for (int j = 0; j < RPT / 2; ++j)
-            *reinterpret_cast<double2*>(p + 2 * j) = make_double2(o[2 * j], o[2 * j + 1]);
-    }
-}
-
-// Fixed-shape block reduction into one partial per lane: the CTA's rows are
-// folded pairwise in a fixed order (deterministic run to run).
-template <int BP, int RPT>
-__device__ __forceinline__ void block_partial(const double (&v)[RPT], double* partial) {
-    constexpr int TPR = BP / RPT, ROWS = kBlock / TPR;
-    __shared__ double sh[kBlock * RPT];  // [ROWS][BP]
-#pragma unroll
-    for (int j = 0; j < RPT; ++j) sh[threadIdx.x * RPT + j] = v[j];
-    __syncthreads();
-#pragma unroll
-    for (int s = ROWS / 2; s >= 1; s >>= 1) {
-        for (int idx = threadIdx.x; idx < s * BP; idx += kBlock) sh[idx] = __dadd_rn(sh[idx], sh[idx + s * BP]);
-        __syncthreads();
-    }
-    for (int idx = threadIdx.x; idx < BP; idx += kBlock)
-        partial[static_cast<int64_t>(blockIdx.x) * BP + idx] = sh[idx];
-}
-
-// Row dot product in the reference order (s = 0.0; s += v_k * x[c_k], per
-// lane) with the loads batched for memory-level parallelism: all column
-// indices and values of the row, then all gathers, then the ordered sums.
-// W = 8 / 2: padded ELL rows (row q at [q*W, q*W+W), padding ci = -1 after
-// the real entries), read with 16-byte vector loads and no row-pointer round
-// trip. W = 0: CSR (rows of up to kMaxRow entries unrolled, longer rows
-// looped). DIAG also returns a_ii and x_ii.
-constexpr int kMaxRow = 8;
-
-template <int W>
-__device__ __forceinline__ void ell_load(const int* __restrict__ eci, const double* __restrict__ ev, int64_t q,
-                                         int (&cc)[kMaxRow], double (&vv)[kMaxRow]) {
-    if constexpr (W == 8) {
-        const int4* cp = reinterpret_cast<const int4*>(eci + q * 8);
-        const int4 c0 = __ldg(cp), c1 = __ldg(cp + 1);
-        cc[0] = c0.x; cc[1] = c0.y; cc[2] = c0.z; cc[3] = c0.w;
-        cc[4] = c1.x; cc[5] = c1.y; cc[6] = c1.z; cc[7] = c1.w;
-        const double2* vp = reinterpret_cast<const double2*>(ev + q * 8);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const double2 t = __ldg(vp + j);
-            vv[2 * j] = t.x;
-            vv[2 * j + 1] = t.y;
-        }
-    } else {  // W == 2
-        const int2 c0 = __ldg(reinterpret_cast<const int2*>(eci + q * 2));
-        const double2 t = __ldg(reinterpret_cast<const double2*>(ev + q * 2));
-        cc[0] = c0.x; cc[1] = c0.y;
-        vv[0] = t.x; vv[1] = t.y;
-#pragma unroll
-        for (int j = 2; j < kMaxRow; ++j) cc[j] = -1;
-    }
-}
-
-template <int RPT, int W, bool DIAG>
-__device__ __forceinline__ void row_dot(const int* __restrict__ rp, const int* __restrict__ ci,
-                                        const double* __restrict__ v, int64_t q,
-                                        const double* __restrict__ x, int nrhs, int lane0, int64_t row,
-                                        double (&s)[RPT], double* d, double (&xr)[RPT]) {
-#pragma unroll
-    for (int l = 0; l < RPT; ++l) s[l] = 0.0;
-    int cc[kMaxRow];
-    double vv[kMaxRow];
-    int len;
-    if constexpr (W > 0) {
-        ell_load<W>(ci, v, q, cc, vv);
-        len = kMaxRow;
-    } else {
-        const int k0 = rp[q];
-        len = rp[q + 1] - k0;
-        if (len > kMaxRow) {  // long row: plain loop
-            for (int k = k0; k < k0 + len; ++k) {
-                const int c = ci[k];
-                const double a = v[k];
-                double xx[RPT];
-                ldv<RPT>(x + static_cast<int64_t>(c) * nrhs + lane0, xx);
-#pragma unroll
-                for (int l = 0; l < RPT; ++l) s[l] = __dadd_rn(s[l], __dmul_rn(a, xx[l]));
-                if (DIAG && c == row) {
-                    *d = a;
-#pragma unroll
-                    for (int l = 0; l < RPT; ++l) xr[l] = xx[l];
-                }
-            }
-            return;
-        }
-#pragma unroll
-        for (int j = 0; j < kMaxRow; ++j) {
-            cc[j] = j < len ? __ldg(ci + k0 + j) : -1;
-            if (j < len) vv[j] = __ldg(v + k0 + j);
-        }
-    }
-    constexpr int MJ = W == 2 ? 2 : kMaxRow;
-    double xv[MJ][RPT];
-#pragma unroll
-    for (int j = 0; j < MJ; ++j)
-        if (cc[j] >= 0) ldv<RPT>(x + static_cast<int64_t>(cc[j]) * nrhs + lane0, xv[j]);
-#pragma unroll
-    for (int j = 0; j < MJ; ++j)
-        if (cc[j] >= 0) {
-#pragma unroll
-            for (int l = 0; l < RPT; ++l) s[l] = __dadd_rn(s[l], __dmul_rn(vv[j], xv[j][l]));
-            if (DIAG && cc[j] == row) {
-                *d = vv[j];
-#pragma unroll
-                for (int l = 0; l < RPT; ++l) xr[l] = xv[j][l];
-            }
-        }
-    (void)len;
-}
-
-#define ROW_SETUP()                                        \
-    constexpr int TPR = BP / RPT;                          \
-    const int64_t t = gtid();                              \
-    const int64_t r = t / TPR;                             \
-    const int lane0 = static_cast<int>(t % TPR) * RPT;
-
-// jacobi_sweep (multigrid.cpp:36-56): s = A x (CSR order),
-// x' = x + (omega (b - s)) / a_ii. x is read entirely before any write
-// (ping-pong buffers), as in the reference, where A.apply fills scratch first.
-template <int BP, int RPT, int W>
-__global__ void __launch_bounds__(kBlock, 2) k_sweep(int n, int nrhs, const int* __restrict__ rp,
-                                                     const int* __restrict__ ci, const double* __restrict__ v,
-                                                     const int* __restrict__ rowid, const double* __restrict__ x,
-                                                     const double* __restrict__ b, double* __restrict__ xo,
-                                                     double omega) {
-    ROW_SETUP();
-    if (r >= n || lane0 >= nrhs) return;
-    const int64_t row = rowid ? rowid[r] : r;
-    const int64_t o = row * nrhs + lane0;
-    double bo[RPT], s[RPT], xr[RPT], out[RPT];
-    ldv<RPT>(b + o, bo);
-    double d = 0.0;
-    row_dot<RPT, W, true>(rp, ci, v, r, x, nrhs, lane0, row, s, &d, xr);
-#pragma unroll
-    for (int l = 0; l < RPT; ++l) out[l] = __dadd_rn(xr[l], __ddiv_rn(__dmul_rn(omega, __dsub_rn(bo[l], s[l])), d));
-    stv<RPT>(xo + o, out);
-}
-
-// First sweep after kernels::fill(0.0, x) (multigrid.cpp:268): A * 0 is
-// exactly +0.0, so x' = 0.0 + (omega (b - 0.0)) / a_ii -- bit-identical to
-// the full sweep without reading the matrix or x.
-template <int BP, int RPT>
-__global__ void __launch_bounds__(kBlock) k_sweep_zero(int n, int nrhs, const double* __restrict__ diag,
-                                                       const double* __restrict__ b, double* __restrict__ xo,
-                                                       double omega) {
-    ROW_SETUP();
-    if (r >= n || lane0 >= nrhs) return;
-    const int64_t o = r * nrhs + lane0;
-    double bo[RPT], out[RPT];
-    ldv<RPT>(b + o, bo);
-    const double dg = diag[r];
-#pragma unroll
-    for (int l = 0; l < RPT; ++l) out[l] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, __dsub_rn(bo[l], 0.0)), dg));
-    stv<RPT>(xo + o, out);
-}
-
-// r = b - A x (multigrid.cpp:263-265 / 317-318); optionally stores r and/or
-// emits per-CTA partial sums of r^2 for the residual norm.
-template <int BP, int RPT, int W, bool STORE>
-__global__ void __launch_bounds__(kBlock, 2) k_residual(int n, int nrhs, const int* __restrict__ rp,
-                                                        const int* __restrict__ ci, const double* __restrict__ v,
-                                                        const int* __restrict__ rowid,
-                                                        const double* __restrict__ x,
-                                                        const double* __restrict__ b, double* __restrict__ rout,
-                                                        double* __restrict__ partial) {
-    ROW_SETUP();
-    const bool valid = r < n && lane0 < nrhs;
-    double rv[RPT];
-#pragma unroll
-    for (int l = 0; l < RPT; ++l) rv[l] = 0.0;
-    if (valid) {
-        const int64_t row = rowid ? rowid[r] : r;
-        const int64_t o = row * nrhs + lane0;
-        double bo[RPT], s[RPT], dummy[RPT];
-        ldv<RPT>(b + o, bo);
-        row_dot<RPT, W, false>(rp, ci, v, r, x, nrhs, lane0, row, s, nullptr, dummy);
-#pragma unroll
-        for (int l = 0; l < RPT; ++l) rv[l] = __dsub_rn(bo[l], s[l]);
-        if (STORE) stv<RPT>(rout + o, rv);
-    }
-    if (partial) {
-        double sq[RPT];
-#pragma unroll
-        for (int l = 0; l < RPT; ++l) sq[l] = __dmul_rn(rv[l], rv[l]);
-        block_partial<BP, RPT>(sq, partial);
-    }
-}
-
-// y = A x over CSR rows (SparseOperator::apply); zero_rows: extension x1
-// (coarse RHS cleared on Dirichlet vertices after restriction).
-template <int BP, int RPT, int W>
-__global__ void __launch_bounds__(kBlock, 2) k_spmv(int nrows, int nrhs, const int* __restrict__ rp,
-                                                    const int* __restrict__ ci, const double* __restrict__ v,
-                                                    const int* __restrict__ rowid, const double* __restrict__ x,
-                                                    double* __restrict__ y, const int* __restrict__ zero_rows) {
-    ROW_SETUP();
-    if (r >= nrows || lane0 >= nrhs) return;
-    const int64_t row = rowid ? rowid[r] : r;
-    double s[RPT], dummy[RPT];
-    row_dot<RPT, W, false>(rp, ci, v, r, x, nrhs, lane0, row, s, nullptr, dummy);
-    if (zero_rows && zero_rows[row]) {
-#pragma unroll
-        for (int l = 0; l < RPT; ++l) s[l] = 0.0;
-    }
-    stv<RPT>(y + row * nrhs + lane0, s);
-}
-
-// x_f += P x_c (multigrid.cpp:277-280); each fine row owns its entry, so the
-// update is in place.
-template <int BP, int RPT, int W>
-__global__ void __launch_bounds__(kBlock, 2) k_prolong_add(int n, int nrhs, const int* __restrict__ rp,
-                                                           const int* __restrict__ ci,
-                                                           const double* __restrict__ v,
-                                                           const int* __restrict__ rowid,
-                                                           const double* __restrict__ xc,
-                                                           double* __restrict__ xf) {
-    ROW_SETUP();
-    if (r >= n || lane0 >= nrhs) return;
-    const int64_t row = rowid ? rowid[r] : r;
-    const int64_t o = row * nrhs + lane0;
-    double xo[RPT], s[RPT], dummy[RPT];
-    ldv<RPT>(xf + o, xo);
-    row_dot<RPT, W, false>(rp, ci, v, r, xc, nrhs, lane0, row, s, nullptr, dummy);
-#pragma unroll
-    for (int l = 0; l < RPT; ++l) xo[l] = __dadd_rn(xo[l], s[l]);
-    stv<RPT>(xf + o, xo);
-}
-
-// ------------------------------------------------------------------------
-// Pipelined persistent row kernel (the hot path on ELL levels).
-//
-// One producer thread streams the index tiles of the reordered operator --
-// kPipeRows rows of ELL column indices, values and original row ids -- into a
-// kPipeStages-deep shared-memory ring with TMA bulk copies (cp.async.bulk +
-// mbarrier complete_tx). 256 consumer threads (kPipeRows = 224 / TPR rows per
-// tile, RPT right-hand sides each) read their row's indices from the ring and
-// issue all x gathers at once: the only memory round trip left on a
-// consumer's critical path is the gather itself. Tiles are
-// assigned statically (tile = blockIdx.x + i * gridDim.x), so every result,
-// including the residual-norm partials, is deterministic for a given grid.
-//
-// OP: 0 sweep (jacobi_sweep), 1 residual store, 2 residual norm partials,
-//     3 y = A x with Dirichlet zero rows (restriction), 4 x += P xc (prolong),
-//     5 sweep that also emits the norm partials of b - A x for the incoming x
-//       (the previous cycle's fine residual; same arithmetic and tile/CTA
-//       partition as op 2, so the norm is bit-identical to a separate pass).
-// 7 consumer warps + 1 producer warp: two CTAs per SM put 4 warps on each
-// SM sub-partition, which leaves 128 registers per thread.
-constexpr int kPipeConsumers = 224;
-constexpr int kPipeThreads = kPipeConsumers + 32;
-constexpr int kPipeStages = 4;
-enum { OP_SWEEP = 0, OP_RES_STORE = 1, OP_RES_NORM = 2, OP_SPMV = 3, OP_PROLONG = 4, OP_SWEEP_NORM = 5 };
-
-struct PipeArgs {
-    int ntiles, nrhs;
-    const int* eci;
-    const double* ev;
-    const int* ord;     // padded: ntiles * rows_per_tile entries, -1 = padding row
-    const double* x;    // gathered vector
-    const double* b;    // OP_SWEEP / OP_RES_*: right-hand side
-    double* out;        // OP_SWEEP: x'; OP_RES_STORE: r; OP_SPMV: y; OP_PROLONG: x_f (in/out)
-    double* partial;    // OP_RES_NORM
-    const int* zero_rows;
-    double omega;
-};
-
-template <int BP, int RPT, int W>
-struct PipeGeom {
-    static constexpr int TPR = BP / RPT;
-    static constexpr int ROWS = kPipeConsumers / TPR;
-    static constexpr uint32_t CI_BYTES = ROWS * W * 4, V_BYTES = ROWS * W * 8, ORD_BYTES = ROWS * 4;
-    static constexpr uint32_t STAGE_BYTES = V_BYTES + CI_BYTES + ORD_BYTES;
-    static constexpr size_t SMEM = static_cast<size_t>(kPipeStages) * STAGE_BYTES;
-};
-
-template <int BP, int RPT, int W, int OP>
-__global__ void __launch_bounds__(kPipeThreads, 2) k_rowop_pipe(PipeArgs a) {
-    using G = PipeGeom<BP, RPT, W>;
-    constexpr int TPR = G::TPR, ROWS = G::ROWS;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t full[kPipeStages], empty[kPipeStages];
-    const int tid = threadIdx.x;
-    if (tid == 0) {
-        for (int s = 0; s < kPipeStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kPipeConsumers / 32);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    // contiguous tile ranges per CTA: spatially adjacent rows (Morton order)
-    // stay on one SM, so the x lines they share are reused from L1
-    const int ntiles = a.ntiles;
-    const int per = (ntiles + gridDim.x - 1) / gridDim.x;
-    const int t_begin = blockIdx.x * per;
-    const int t_end = t_begin + per < ntiles ? t_begin + per : ntiles;
-    double acc[RPT];
-#pragma unroll
-    for (int l = 0; l < RPT; ++l) acc[l] = 0.0;
-
-    if (tid >= kPipeConsumers) {
-        if (tid == kPipeConsumers) {  // producer
-            int i = 0;
-            for (int t = t_begin; t < t_end; ++t, ++i) {
-                const int s = i % kPipeStages;
-                if (i >= kPipeStages) mbar_wait(&empty[s], ((i / kPipeStages) - 1) & 1);
-                unsigned char* st = smem_raw + static_cast<size_t>(s) * G::STAGE_BYTES;
-                mbar_expect_tx(&full[s], G::STAGE_BYTES);
-                tma_bulk_g2s(st, a.ev + static_cast<int64_t>(t) * ROWS * W, G::V_BYTES, &full[s]);
-                tma_bulk_g2s(st + G::V_BYTES, a.eci + static_cast<int64_t>(t) * ROWS * W, G::CI_BYTES, &full[s]);
-                tma_bulk_g2s(st + G::V_BYTES + G::CI_BYTES, a.ord + static_cast<int64_t>(t) * ROWS, G::ORD_BYTES,
-                             &full[s]);
-            }
-        }
-    } else {
-        const int q = tid / TPR;
-        const int lane0 = (tid % TPR) * RPT;
-        const int nrhs = a.nrhs;
-        int i = 0;
-        for (int t = t_begin; t < t_end; ++t, ++i) {
-            const int s = i % kPipeStages;
-            mbar_wait(&full[s], (i / kPipeStages) & 1);
-            const unsigned char* st = smem_raw + static_cast<size_t>(s) * G::STAGE_BYTES;
-            const double* vs = reinterpret_cast<const double*>(st);
-            const int* cs = reinterpret_cast<const int*>(st + G::V_BYTES);
-            const int* os = reinterpret_cast<const int*>(st + G::V_BYTES + G::CI_BYTES);
-            // indices and values are read straight from the stage (kept until
-            // the tile is done), so registers hold only the gathered x values
-            const int* cq = cs + q * W;
-            const double* vq = vs + q * W;
-            const int row32 = os[q];
-            const bool active = row32 >= 0 && lane0 < nrhs;
-            const int64_t row = row32;
-            const int64_t o = row * nrhs + lane0;
-            double pre[RPT], xv[W][RPT], sum[RPT], xr[RPT], d = 0.0;
-            if (active) {
-                if constexpr (OP == OP_SWEEP || OP == OP_SWEEP_NORM || OP == OP_RES_STORE || OP == OP_RES_NORM)
-                    ldv<RPT>(a.b + o, pre);
-                if constexpr (OP == OP_PROLONG) ldv<RPT>(a.out + o, pre);
-#pragma unroll
-                for (int j = 0; j < W; ++j) {
-                    const int cj = cq[j];
-                    if (cj >= 0) ldv<RPT>(a.x + static_cast<int64_t>(cj) * nrhs + lane0, xv[j]);
-                }
-#pragma unroll
-                for (int l = 0; l < RPT; ++l) sum[l] = 0.0;
-#pragma unroll
-                for (int j = 0; j < W; ++j) {
-                    const int cj = cq[j];
-                    if (cj >= 0) {
-                        const double vj = vq[j];
-#pragma unroll
-                        for (int l = 0; l < RPT; ++l) sum[l] = __dadd_rn(sum[l], __dmul_rn(vj, xv[j][l]));
-                        if ((OP == OP_SWEEP || OP == OP_SWEEP_NORM) && cj == row32) d = vj;
-                    }
-                }
-                // x_ii: re-read (an L1 hit -- the diagonal gather just brought it in)
-                if constexpr (OP == OP_SWEEP || OP == OP_SWEEP_NORM) ldv<RPT>(a.x + o, xr);
-            }
-            __syncwarp();
-            if ((tid & 31) == 0) mbar_arrive(&empty[s]);  // stage consumed
-            if (!active) continue;
-            double res[RPT];
-#pragma unroll
-            for (int l = 0; l < RPT; ++l) {
-                if constexpr (OP == OP_SWEEP_NORM) {
-                    const double rl = __dsub_rn(pre[l], sum[l]);
-                    acc[l] = __dadd_rn(acc[l], __dmul_rn(rl, rl));
-                }
-                if constexpr (OP == OP_SWEEP || OP == OP_SWEEP_NORM)
-                    res[l] = __dadd_rn(xr[l], __ddiv_rn(__dmul_rn(a.omega, __dsub_rn(pre[l], sum[l])), d));
-                else if constexpr (OP == OP_RES_STORE || OP == OP_RES_NORM)
-                    res[l] = __dsub_rn(pre[l], sum[l]);
-                else if constexpr (OP == OP_PROLONG)
-                    res[l] = __dadd_rn(pre[l], sum[l]);
-                else
-                    res[l] = sum[l];
-            }
-            if constexpr (OP == OP_SPMV) {
-                if (a.zero_rows && a.zero_rows[row]) {
-#pragma unroll
-                    for (int l = 0; l < RPT; ++l) res[l] = 0.0;
-                }
-            }
-            if constexpr (OP == OP_RES_NORM) {
-#pragma unroll
-                for (int l = 0; l < RPT; ++l) acc[l] = __dadd_rn(acc[l], __dmul_rn(res[l], res[l]));
-            } else {
-                stv<RPT>(a.out + o, res);
-            }
-        }
-    }
-    if constexpr (OP == OP_RES_NORM || OP == OP_SWEEP_NORM) {
-        // fold the consumers' accumulators: [ROWS][BP] in a fixed tree order,
-        // rows padded with zeros to a power of two (ROWS = 224 / TPR is not one)
-        constexpr int RP2 = ROWS <= 1 ? 1 : (ROWS <= 2 ? 2 : (ROWS <= 4 ? 4 : (ROWS <= 8 ? 8 : (ROWS <= 16 ? 16 :
-                            (ROWS <= 32 ? 32 : (ROWS <= 64 ? 64 : (ROWS <= 128 ? 128 : 256)))))));
-        __shared__ double sh[RP2 * BP];
-        for (int idx = kPipeConsumers * RPT + tid; idx < RP2 * BP; idx += kPipeThreads) sh[idx] = 0.0;
-        if (tid < kPipeConsumers)
-#pragma unroll
-            for (int l = 0; l < RPT; ++l) sh[tid * RPT + l] = acc[l];
-        __syncthreads();
-        for (int sft = RP2 / 2; sft >= 1; sft >>= 1) {
-            for (int idx = tid; idx < sft * BP; idx += kPipeThreads) sh[idx] = __dadd_rn(sh[idx], sh[idx + sft * BP]);
-            __syncthreads();
-        }
-        for (int idx = tid; idx < BP; idx += kPipeThreads)
-            a.partial[static_cast<int64_t>(blockIdx.x) * BP + idx] = sh[idx];
-    }
-}
-
-// partials of b_i^2
-template <int BP, int RPT>
-__global__ void __launch_bounds__(kBlock) k_sumsq(int n, int nrhs, const double* __restrict__ b,
-                                                  double* __restrict__ partial) {
-    ROW_SETUP();
-    double sq[RPT];
-#pragma unroll
-    for (int l = 0; l < RPT; ++l) sq[l] = 0.0;
-    if (r < n && lane0 < nrhs) {
-        double bv[RPT];
-        ldv<RPT>(b + r * nrhs + lane0, bv);
-#pragma unroll
-        for (int l = 0; l < RPT; ++l) sq[l] = __dmul_rn(bv[l], bv[l]);
-    }
-    block_partial<BP, RPT>(sq, partial);
-}
-
-// Partials are folded by repeated fixed-shape block reductions (each CTA folds
-// 256/BP consecutive partial rows), then finalized:
-// mode 0: out[lane] = total
-// mode 1: out[lane] = sqrt(total)                      (norm)
-// mode 2: out[lane] = sqrt(total) / denom[lane]         (relative residual)
-template <int BP>
-__global__ void __launch_bounds__(kBlock) k_fold(int64_t nrows, const double* __restrict__ in,
-                                                 double* __restrict__ out) {
-    const int64_t t = gtid();
-    const int64_t row = t / BP;
-    const int lane = static_cast<int>(t % BP);
-    const double val[1] = {row < nrows ? in[row * BP + lane] : 0.0};
-    block_partial<BP, 1>(val, out);
-}
-
-__global__ void k_finalize(int nrhs, const double* __restrict__ tot, double* __restrict__ out, int mode,
-                           const double* __restrict__ denom) {
-    const int lane = threadIdx.x;
-    if (lane >= nrhs) return;
-    const double t = tot[lane];
-    if (mode == 0) out[lane] = t;
-    else if (mode == 1) out[lane] = __dsqrt_rn(t);
-    else out[lane] = __ddiv_rn(__dsqrt_rn(t), denom[lane]);
-}
-
-__global__ void k_denom(int nrhs, const double* __restrict__ bn, double* __restrict__ denom) {
-    const int l = threadIdx.x;
-    if (l < nrhs) denom[l] = bn[l] > 0.0 ? bn[l] : 1.0;
-}
-
-// project_compatible sums (multigrid.cpp:240-250), in the reference's exact
-// order: `mean += w[i] * b[i]; total += w[i];` for i ascending, one lane per
-// right-hand side. A constant offset in b lies outside range(L), so any other
-// summation order leaves a permanent residual floor of a few ulps * sqrt(n)
-// that would show up in the per-cycle history; this keeps it bit-identical.
-//
-// The sum is a dependent add chain, so the kernel is built to run at the
-// DADD latency: one producer thread streams [CH rows x nrhs] tiles of b and
-// the matching w tiles into a kStages-deep shared-memory ring with TMA bulk
-// copies (cp.async.bulk + mbarrier complete_tx), and warp 0 consumes them.
-constexpr int kProjStages = 4;
-constexpr int kProjRows = 128;
-
-__global__ void __launch_bounds__(64) k_project_sums(int n, int nrhs, const double* __restrict__ w,
-                                                     const double* __restrict__ b,
-                                                     double* __restrict__ mean_out) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    double* bbuf = reinterpret_cast<double*>(smem_raw);                       // [S][CH*nrhs]
-    double* wbuf = bbuf + static_cast<size_t>(kProjStages) * kProjRows * nrhs;  // [S][CH]
-    __shared__ __align__(8) uint64_t full[kProjStages], empty[kProjStages];
-    const int nchunks = n / kProjRows;  // full tiles; the tail is read directly
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kProjStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (threadIdx.x == 32) {
-        // producer
-        const uint32_t bbytes = kProjRows * nrhs * sizeof(double), wbytes = kProjRows * sizeof(double);
-        for (int c = 0; c < nchunks; ++c) {
-            const int s = c % kProjStages;
-            if (c >= kProjStages) mbar_wait(&empty[s], ((c / kProjStages) - 1) & 1);
-            mbar_expect_tx(&full[s], bbytes + wbytes);
-            tma_bulk_g2s(bbuf + static_cast<size_t>(s) * kProjRows * nrhs,
-                         b + static_cast<int64_t>(c) * kProjRows * nrhs, bbytes, &full[s]);
-            tma_bulk_g2s(wbuf + s * kProjRows, w + static_cast<int64_t>(c) * kProjRows, wbytes, &full[s]);
-        }
-    } else if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        double mean = 0.0, total = 0.0;
-        for (int c = 0; c < nchunks; ++c) {
-            const int s = c % kProjStages;
-            mbar_wait(&full[s], (c / kProjStages) & 1);
-            const double* bt = bbuf + static_cast<size_t>(s) * kProjRows * nrhs;
-            const double* wt = wbuf + s * kProjRows;
-            if (lane < nrhs) {
-                // products first (independent), then the dependent add chains
-                for (int i0 = 0; i0 < kProjRows; i0 += 16) {
-                    double p[16], wv[16];
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) {
-                        wv[u] = wt[i0 + u];
-                        p[u] = __dmul_rn(wv[u], bt[(i0 + u) * nrhs + lane]);
-                    }
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) {
-                        mean = __dadd_rn(mean, p[u]);
-                        total = __dadd_rn(total, wv[u]);
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-        }
-        if (lane < nrhs) {
-            for (int i = nchunks * kProjRows; i < n; ++i) {
-                const double wv = w[i];
-                mean = __dadd_rn(mean, __dmul_rn(wv, b[static_cast<int64_t>(i) * nrhs + lane]));
-                total = __dadd_rn(total, wv);
-            }
-            mean_out[lane] = __ddiv_rn(mean, total);
-        }
-    }
-}
-
-// b -= mean (per right-hand side)
-template <int BP>
-__global__ void __launch_bounds__(kBlock) k_project(int n, int nrhs, const double* __restrict__ mean,
-                                                    double* __restrict__ b) {
-    const int64_t t = gtid();
-    const int64_t row = t / BP;
-    const int lane = static_cast<int>(t % BP);
-    if (row >= n || lane >= nrhs) return;
-    const int64_t o = row * nrhs + lane;
-    b[o] = __dsub_rn(b[o], mean[lane]);
-}
-
-// Coarse solve: the projected weighted CG of oracle/ref_standin_direct.cpp,
-// one thread per right-hand side, sequential dots -- bit-identical to the
-// CPU stand-in. Dirichlet (x1): same CG without the two projections.
-__global__ void k_coarse_cg(int n, int nrhs, const int* __restrict__ rp, const int* __restrict__ ci,
-                            const double* __restrict__ v, const double* __restrict__ w, double wtot,
-                            int project, const double* __restrict__ b, double* __restrict__ x,
-                            double* __restrict__ scratch) {
-    const int lane = threadIdx.x;
-    if (lane >= nrhs) return;
-    double* r = scratch + static_cast<int64_t>(lane) * 4 * n;
-    double* p = r + n;
-    double* Ap = p + n;
-    double* xl = Ap + n;
-    if (project) {
-        double m = 0.0;
-        for (int i = 0; i < n; ++i) m = __dadd_rn(m, __dmul_rn(w[i], b[static_cast<int64_t>(i) * nrhs + lane]));
-        m = __ddiv_rn(m, wtot);
-        for (int i = 0; i < n; ++i) r[i] = __dsub_rn(b[static_cast<int64_t>(i) * nrhs + lane], m);
-    } else {
-        for (int i = 0; i < n; ++i) r[i] = b[static_cast<int64_t>(i) * nrhs + lane];
-    }
-    for (int i = 0; i < n; ++i) {
-        xl[i] = 0.0;
-        p[i] = r[i];
-    }
-    double rr = 0.0;
-    for (int i = 0; i < n; ++i) rr = __dadd_rn(rr, __dmul_rn(__dmul_rn(w[i], r[i]), r[i]));
-    const double rr0 = rr;
-    const int maxit = 4 * n + 20;
-    for (int it = 0; it < maxit; ++it) {
-        if (!(rr > __dmul_rn(1e-30, rr0))) break;
-        for (int i = 0; i < n; ++i) {
-            double s = 0.0;
-            for (int k = rp[i]; k < rp[i + 1]; ++k) s = __dadd_rn(s, __dmul_rn(v[k], p[ci[k]]));
-            Ap[i] = s;
-        }
-        double curv = 0.0;
-        for (int i = 0; i < n; ++i) curv = __dadd_rn(curv, __dmul_rn(__dmul_rn(w[i], p[i]), Ap[i]));
-        if (curv == 0.0) break;
-        const double alpha = __ddiv_rn(rr, curv);
-        for (int i = 0; i < n; ++i) xl[i] = __dadd_rn(xl[i], __dmul_rn(alpha, p[i]));
-        for (int i = 0; i < n; ++i) r[i] = __dsub_rn(r[i], __dmul_rn(alpha, Ap[i]));
-        double rn = 0.0;
-        for (int i = 0; i < n; ++i) rn = __dadd_rn(rn, __dmul_rn(__dmul_rn(w[i], r[i]), r[i]));
-        const double beta = __ddiv_rn(rn, rr);
-        for (int i = 0; i < n; ++i) p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
-        rr = rn;
-    }
-    double ym = 0.0;
-    if (project) {
-        for (int i = 0; i < n; ++i) ym = __dadd_rn(ym, __dmul_rn(w[i], xl[i]));
-        ym = __ddiv_rn(ym, wtot);
-    }
-    for (int i = 0; i < n; ++i)
-        x[static_cast<int64_t>(i) * nrhs + lane] = project ? __dsub_rn(xl[i], ym) : xl[i];
-}
-
-// Copy the columns (RHS lanes) selected by mask from src to dst.
-__global__ void k_copy_lanes(int64_t total, int nrhs, unsigned mask, const double* __restrict__ src,
-                             double* __restrict__ dst) {
-    const int64_t t = gtid();
-    if (t >= total) return;
-    const int lane = static_cast<int>(t % nrhs);
-    if (mask & (1u << lane)) dst[t] = src[t];
-}
-
-// ------------------------------------------------------------- dispatch ----
-inline int bp_of(int nrhs) {
-    int bp = 1;
-    while (bp < nrhs) bp *= 2;
-    return bp;
-}
-
-// (BP, RPT) instantiations, key = 10 * BP + RPT. RPT > 1 (16-byte vector
-// mapping) only when nrhs == BP >= 2.
-#define DISPATCH_BP(key, ...)                                                    \
-    switch (key) {                                                              \
-        case 11: { constexpr int BP = 1, RPT = 1; __VA_ARGS__; break; }         \
-        case 21: { constexpr int BP = 2, RPT = 1; __VA_ARGS__; break; }         \
-        case 41: { constexpr int BP = 4, RPT = 1; __VA_ARGS__; break; }         \
-        case 81: { constexpr int BP = 8, RPT = 1; __VA_ARGS__; break; }         \
-        case 161: { constexpr int BP = 16, RPT = 1; __VA_ARGS__; break; }       \
-        case 321: { constexpr int BP = 32, RPT = 1; __VA_ARGS__; break; }       \
-        case 22: { constexpr int BP = 2, RPT = 2; __VA_ARGS__; break; }         \
-        case 42: { constexpr int BP = 4, RPT = 2; __VA_ARGS__; break; }         \
-        case 44: { constexpr int BP = 4, RPT = 4; __VA_ARGS__; break; }         \
-        case 82: { constexpr int BP = 8, RPT = 2; __VA_ARGS__; break; }         \
-        case 84: { constexpr int BP = 8, RPT = 4; __VA_ARGS__; break; }         \
-        case 162: { constexpr int BP = 16, RPT = 2; __VA_ARGS__; break; }       \
-        case 164: { constexpr int BP = 16, RPT = 4; __VA_ARGS__; break; }       \
-        case 322: { constexpr int BP = 32, RPT = 2; __VA_ARGS__; break; }       \
-        default: { constexpr int BP = 32, RPT = 4; __VA_ARGS__; break; }        \
-    }
-#define DISPATCH_B1(bp, ...)                                                    \
-    switch (bp) {                                                               \
-        case 1: { constexpr int BP = 1; __VA_ARGS__; break; }                   \
-        case 2: { constexpr int BP = 2; __VA_ARGS__; break; }                   \
-        case 4: { constexpr int BP = 4; __VA_ARGS__; break; }                   \
-        case 8: { constexpr int BP = 8; __VA_ARGS__; break; }                   \
-        case 16: { constexpr int BP = 16; __VA_ARGS__; break; }                 \
-        default: { constexpr int BP = 32; __VA_ARGS__; break; }                 \
-    }
-
-enum Cls { kFineSweep = 0, kFineResidual = 1, kRestrict = 2, kProlong = 3, kCoarseLevels = 4,
-           kCoarseSolve = 5, kNorms = 6, kZeroSweep = 7 };
 
 // Dispatch the pipelined kernel on the ELL width of an operator (7 or 8).
 #define PIPE_W(w, OP, ...) ((w) == 7 ? pipe<OP, 7>(__VA_ARGS__) : pipe<OP, 8>(__VA_ARGS__))
