@@ -164,6 +164,32 @@ DECMG_API int decmg_base_mesh(const char* spec, double* positions, int* nv, int*
  * RHS j uses seed + j. Writes [n0][nrhs]. Dirichlet contexts zero boundary rows. */
 DECMG_API int decmg_gpu_make_rhs(decmg_gpu_ctx* ctx, const char* kind, uint64_t seed, int nrhs, double* b);
 
+
+/* ---- Vertex-partitioned multi-GPU V-cycle ----
+ * Every rank builds the full hierarchy; levels with >= agglomerate_below
+ * vertices per rank are partitioned by Morton-key ranges with 1-ring halos
+ * (NCCL grouped send/recv), coarser levels run replicated on every rank.
+ * Iterates are bit-identical to the single-GPU solve for any rank count.
+ * nccl_id == NULL: emulate world_size ranks inside this process on
+ * cfg->device (device copies instead of NCCL; used by the parity tests).
+ * Otherwise one process per GPU: rank in [0, world_size), nccl_id = the
+ * 128-byte ncclUniqueId from decmg_gpu_nccl_unique_id on rank 0. */
+typedef struct decmg_gpu_dist decmg_gpu_dist;
+DECMG_API int decmg_gpu_nccl_unique_id(void* out, int bytes);
+DECMG_API int decmg_gpu_dist_create(const double* positions, int nv, const int* corner_triples, int nt, int nsub,
+                                    unsigned flags, const decmg_gpu_config* cfg, int world_size, int rank,
+                                    const void* nccl_id, int agglomerate_below, decmg_gpu_dist** out);
+DECMG_API void decmg_gpu_dist_destroy(decmg_gpu_dist* d);
+DECMG_API const char* decmg_gpu_dist_last_error(const decmg_gpu_dist* d);
+DECMG_API int decmg_gpu_dist_info(const decmg_gpu_dist* d, int* agglomeration_level, int* levels, int64_t* owned0,
+                                  int64_t* halo0);
+/* run_cycle (solve == 0, ncycles = max_cycles) or gmg_solve (solve != 0) with
+ * full-length host vectors replicated on every rank; x_out receives the full
+ * solution on every rank. */
+DECMG_API int decmg_gpu_dist_run(decmg_gpu_dist* d, const decmg_gpu_plan* plan, int nrhs, const double* b,
+                                 const double* x0, int max_cycles, int solve, double tol, double* x_out,
+                                 double* hist_out, int* cycles_done, double* final_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,9 +6,10 @@ C ABI in include/decmg_gpu.h). This package is the host-side mirror of the
 reference's C++ multigrid API; it has no CPU implementation of the path.
 """
 from ._lib import DecmgError, CudaError, LIB_PATH, load as load_library
-from .multigrid import (CycleKind, CyclePlan, CycleResult, MultigridHierarchy, Smoother, SmootherConfig,
-                        SolveReport, Transition, base_mesh, build_hierarchy, gmg_solve, standard_plan)
+from .multigrid import (CycleKind, CyclePlan, CycleResult, DistributedHierarchy, MultigridHierarchy, Smoother,
+                        SmootherConfig, SolveReport, Transition, base_mesh, build_hierarchy, gmg_solve,
+                        nccl_unique_id, standard_plan)
 
-__all__ = ["CycleKind", "CyclePlan", "CycleResult", "MultigridHierarchy", "Smoother", "SmootherConfig",
+__all__ = ["CycleKind", "CyclePlan", "CycleResult", "DistributedHierarchy", "MultigridHierarchy", "nccl_unique_id", "Smoother", "SmootherConfig",
            "SolveReport", "Transition", "base_mesh", "build_hierarchy", "gmg_solve", "standard_plan",
            "DecmgError", "CudaError", "LIB_PATH", "load_library"]

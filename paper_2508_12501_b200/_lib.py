@@ -80,6 +80,16 @@ SIGNATURES = {
     "decmg_gpu_launch_count": (C.c_int64, [C.c_void_p]),
     "decmg_base_mesh": (C.c_int, [C.c_char_p, C.c_void_p, C.POINTER(C.c_int), C.c_void_p, C.POINTER(C.c_int)]),
     "decmg_gpu_make_rhs": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_int, C.c_void_p]),
+    "decmg_gpu_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_int]),
+    "decmg_gpu_dist_create": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_uint,
+                                        C.POINTER(decmg_gpu_config), C.c_int, C.c_int, C.c_void_p, C.c_int,
+                                        C.POINTER(C.c_void_p)]),
+    "decmg_gpu_dist_destroy": (None, [C.c_void_p]),
+    "decmg_gpu_dist_last_error": (C.c_char_p, [C.c_void_p]),
+    "decmg_gpu_dist_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_int64)]),
+    "decmg_gpu_dist_run": (C.c_int, [C.c_void_p, C.POINTER(decmg_gpu_plan), C.c_int, C.c_void_p, C.c_void_p,
+                                     C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 
 _lib = None
@@ -107,9 +117,9 @@ _EXC = {DECMG_INVALID_ARGUMENT: ValueError, DECMG_RUNTIME: RuntimeError, DECMG_C
         DECMG_NCCL: DecmgError, DECMG_OOM: MemoryError}
 
 
-def check(rc: int, ctx=None) -> None:
+def check(rc: int, ctx=None, dist=False) -> None:
     if rc == DECMG_OK:
         return
-    msg = load().decmg_gpu_last_error(ctx)
+    msg = (load().decmg_gpu_dist_last_error if dist else load().decmg_gpu_last_error)(ctx)
     msg = msg.decode() if msg else f"decmg_gpu error {rc}"
     raise _EXC.get(rc, DecmgError)(msg)

@@ -186,6 +186,9 @@ Status build_from_levels(decmg_gpu_ctx* c, const decmg_gpu_level_desc* levels, i
                          unsigned flags);
 Status alloc_work(decmg_gpu_ctx* c);
 Status exclusive_scan(decmg_gpu_ctx* c, const int* in, int* out, int n);  // out[n] = total
+Status level_bbox(decmg_gpu_ctx* c, const Level& m, double lo[3], double sc[3]);
+Status morton_keys(decmg_gpu_ctx* c, const Level& m, const double lo[3], const double sc[3],
+                   unsigned long long* d_keys, int* d_id);
 
 // cycle.cu
 struct Plan {

@@ -19,7 +19,7 @@
 // so sweeps, residuals and transfers are bit-identical to the reference.
 // Norms and projections use a fixed-shape tree reduction: deterministic run
 // to run, within a few ulps of the reference's blocked sums.
-#include "rowkernels.cuh"
+#include "driver.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -27,305 +27,6 @@
 
 namespace decmg_gpu {
 namespace {
-
-// Dispatch the pipelined kernel on the ELL width of an operator (7 or 8).
-#define PIPE_W(w, OP, ...) ((w) == 7 ? pipe<OP, 7>(__VA_ARGS__) : pipe<OP, 8>(__VA_ARGS__))
-
-struct Driver {
-    decmg_gpu_ctx* c;
-    int nrhs, bp;
-    const double* b0;  // level-0 right-hand side
-    int key = 0;       // DISPATCH_BP key of the row kernels (10 * BP + RPT)
-    int tpr = 1;       // threads per row
-    // Fused residual norm: when set, the next level-0 sweep also writes
-    // ||b - A x|| / denom of the x it reads into fuse_hist, then calls
-    // fuse_hook(xprev, &stop); stop == true undoes the sweep's buffer flip and
-    // abandons the rest of the cycle (gmg_solve's convergence exit).
-    double* fuse_hist = nullptr;
-    const double* fuse_denom = nullptr;
-    std::function<Status(const double*, bool*)> fuse_hook;
-    bool stopped = false;
-
-    void init() {
-        const bool vec = nrhs == bp && bp >= 2;
-        int rpt = vec ? (bp < c->rpt ? bp : c->rpt) : 1;
-        key = 10 * bp + rpt;
-        tpr = bp / rpt;
-    }
-
-    const double* bptr(int k) const { return k == 0 ? b0 : c->lv[k].b; }
-    static double* xcur(Level& L) { return L.x[L.cur]; }
-
-    unsigned rows_grid(int n) const { return grid_for(static_cast<int64_t>(n) * tpr, kBlock); }
-
-    // Launch the pipelined persistent row kernel on an ELL operator.
-    // Returns the grid size in *grid (the number of norm partials for OP_RES_NORM).
-    template <int OP, int W>
-    Status pipe(int cls, double bytes, int nrows, const int* eci, const double* ev, const int* erow,
-                const double* x, const double* b, double* out, double* partial, const int* zr, double omega,
-                int* grid = nullptr) {
-        Status st;
-        DISPATCH_BP(key, {
-            using G = PipeGeom<BP, RPT, W>;
-            static_assert((G::ROWS * 4 % 16 == 0 && G::CI_BYTES % 16 == 0) || BP / RPT > 8, "pipe tile");
-            const int ntiles = (nrows + G::ROWS - 1) / G::ROWS;
-            const int g = ntiles < 2 * c->num_sms ? ntiles : 2 * c->num_sms;
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(k_rowop_pipe<BP, RPT, W, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(G::SMEM));
-                attr = true;
-            }
-            PipeArgs a{ntiles, nrhs, eci, ev, erow, x, b, out, partial, zr, omega};
-            st = launch(c, cls, bytes, [&] {
-                k_rowop_pipe<BP, RPT, W, OP><<<g, kPipeThreads, G::SMEM, c->stream>>>(a);
-            });
-            if (grid) *grid = g;
-        })
-        return st;
-    }
-
-    Status ensure_x(int k) {
-        Level& L = c->lv[k];
-        if (L.x_zero) {
-            DG_CUDA(cudaMemsetAsync(xcur(L), 0, sizeof(double) * L.nv * nrhs, c->stream));
-            L.x_zero = false;
-        }
-        return Status::Ok();
-    }
-
-    Status smooth(int k, int iters, const Plan& plan) {
-        Level& L = c->lv[k];
-        if (iters <= 0) return Status::Ok();
-        if (L.zero_diag_row >= 0)
-            return Status::Err(DECMG_RUNTIME, "jacobi: zero diagonal at row " + std::to_string(L.zero_diag_row));
-        const double R = nrhs;
-        for (int it = 0; it < iters; ++it) {
-            double* xo = L.x[L.cur ^ 1];
-            const double* b = bptr(k);
-            if (L.x_zero) {
-                const double bytes = 8.0 * L.nv + 16.0 * L.nv * R;
-                DG_TRY(launch(c, kZeroSweep, bytes, [&] {
-                    DISPATCH_BP(key, k_sweep_zero<BP, RPT><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                        L.nv, nrhs, L.diag, b, xo, plan.omega));
-                }));
-            } else {
-                const double bytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
-                const double* x = xcur(L);
-                if (k == 0 && it == 0 && fuse_hist && L.Le_ci && tpr <= 8) {
-                    int g = 0;
-                    DG_TRY(PIPE_W(L.Le_w, OP_SWEEP_NORM, kFineSweep, bytes, L.nv, L.Le_ci, L.Le_v, L.Le_row, x, b,
-                                  xo, c->red, nullptr, plan.omega, &g));
-                    DG_TRY(reduce_partials(g, fuse_hist, 2, fuse_denom));
-                    fuse_hist = nullptr;
-                    L.cur ^= 1;
-                    L.x_zero = false;
-                    if (fuse_hook) {
-                        bool stop = false;
-                        DG_TRY(fuse_hook(L.x[L.cur ^ 1], &stop));
-                        if (stop) {
-                            L.cur ^= 1;  // x_prev stays the current iterate
-                            stopped = true;
-                            return Status::Ok();
-                        }
-                    }
-                    continue;
-                } else if (L.Le_ci && tpr <= 8) {
-                    DG_TRY(PIPE_W(L.Le_w, OP_SWEEP, k == 0 ? kFineSweep : kCoarseLevels, bytes, L.nv, L.Le_ci,
-                                  L.Le_v, L.Le_row, x, b, xo, nullptr, nullptr, plan.omega, nullptr));
-                } else {
-                    DG_TRY(launch(c, k == 0 ? kFineSweep : kCoarseLevels, bytes, [&] {
-                        DISPATCH_BP(key, (k_sweep<BP, RPT, 0><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                            L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b, xo, plan.omega)))
-                    }));
-                }
-            }
-            L.cur ^= 1;
-            L.x_zero = false;
-        }
-        return Status::Ok();
-    }
-
-    // r = b - A x on level k, then b_{k+1} = R r (multigrid.cpp:263-267)
-    Status residual_restrict(int k) {
-        DG_TRY(ensure_x(k));
-        Level& L = c->lv[k];
-        Level& C = c->lv[k + 1];
-        const double R = nrhs;
-        const double* x = xcur(L);
-        const double* b = bptr(k);
-        const double rbytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
-        if (L.Le_ci && tpr <= 8) {
-            DG_TRY(PIPE_W(L.Le_w, OP_RES_STORE, k == 0 ? kFineResidual : kCoarseLevels, rbytes, L.nv, L.Le_ci,
-                          L.Le_v, L.Le_row, x, b, c->r, nullptr, nullptr, 0.0, nullptr));
-        } else {
-            DG_TRY(launch(c, k == 0 ? kFineResidual : kCoarseLevels, rbytes, [&] {
-                DISPATCH_BP(key, (k_residual<BP, RPT, 0, true><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                    L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b, c->r, nullptr)))
-            }));
-        }
-        const double tbytes = 12.0 * L.nnzR + 4.0 * (C.nv + 1) + 8.0 * L.nv * R + 8.0 * C.nv * R;
-        const int* zr = c->dirichlet ? C.bd : nullptr;
-        if (L.Re_ci && tpr <= 8) {
-            DG_TRY(PIPE_W(L.Re_w, OP_SPMV, k == 0 ? kRestrict : kCoarseLevels, tbytes, C.nv, L.Re_ci, L.Re_v,
-                          L.Re_row, c->r, nullptr, C.b, nullptr, zr, 0.0, nullptr));
-        } else {
-            DG_TRY(launch(c, k == 0 ? kRestrict : kCoarseLevels, tbytes, [&] {
-                DISPATCH_BP(key, (k_spmv<BP, RPT, 0><<<rows_grid(C.nv), kBlock, 0, c->stream>>>(
-                                    C.nv, nrhs, L.Ro_rp, L.Ro_ci, L.Ro_v, C.ord, c->r, C.b, zr)))
-            }));
-        }
-        return Status::Ok();
-    }
-
-    // x_k += P_k x_{k+1}
-    Status prolong(int k) {
-        DG_TRY(ensure_x(k));
-        DG_TRY(ensure_x(k + 1));
-        Level& L = c->lv[k];
-        Level& C = c->lv[k + 1];
-        const double R = nrhs;
-        const double bytes = 12.0 * L.nnzP + 4.0 * (L.nv + 1) + 8.0 * C.nv * R + 16.0 * L.nv * R;
-        const double* xc = xcur(C);
-        double* xf = xcur(L);
-        if (L.Pe_ci && tpr <= 8) {
-            DG_TRY((pipe<OP_PROLONG, 2>(k == 0 ? kProlong : kCoarseLevels, bytes, L.nv, L.Pe_ci, L.Pe_v, L.Le_row,
-                                        xc, nullptr, xf, nullptr, nullptr, 0.0)));
-        } else {
-            DG_TRY(launch(c, k == 0 ? kProlong : kCoarseLevels, bytes, [&] {
-                DISPATCH_BP(key, (k_prolong_add<BP, RPT, 0><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                    L.nv, nrhs, L.Po_rp, L.Po_ci, L.Po_v, L.ord, xc, xf)))
-            }));
-        }
-        return Status::Ok();
-    }
-
-    Status coarse_solve(int k) {
-        Level& L = c->lv[k];
-        double* x = xcur(L);
-        const double* b = bptr(k);
-        const int project = c->dirichlet ? 0 : 1;
-        DG_TRY(launch(c, kCoarseSolve, 0.0, [&] {
-            k_coarse_cg<<<1, 32, 0, c->stream>>>(L.nv, nrhs, L.L_rp, L.L_ci, L.L_v, L.area, L.wtot,
-                                                 project, b, x, c->coarse_scratch);
-        }));
-        L.x_zero = false;
-        return Status::Ok();
-    }
-
-    // MultigridHierarchy::cycle_once (multigrid.cpp:252-285)
-    Status cycle_once(const Plan& plan) {
-        const int nw = static_cast<int>(plan.walk.size());
-        const int Lc = static_cast<int>(c->lv.size());
-        int level = 0;
-        for (int w = 0; w < nw; ++w) {
-            if (plan.walk[w] == 'd') {
-                DG_TRY(smooth(level, plan.pre[level], plan));
-                if (stopped) return Status::Ok();
-                DG_TRY(residual_restrict(level));
-                ++level;
-                c->lv[level].x_zero = true;  // kernels::fill(0.0, xs[level])
-                if (level == Lc - 1) {
-                    DG_TRY(coarse_solve(level));
-                } else if (w + 1 < nw && plan.walk[w + 1] == 'u') {
-                    DG_TRY(smooth(level, plan.pre[level], plan));
-                }
-            } else {
-                DG_TRY(prolong(level - 1));
-                --level;
-                DG_TRY(smooth(level, plan.post[level], plan));
-            }
-        }
-        return Status::Ok();
-    }
-
-    int partial_blocks(int n) const { return static_cast<int>(rows_grid(n)); }
-
-    // Fold nrows partial rows ([nrows][bp] in c->red) down to one row.
-    Status reduce_partials(int64_t nrows, double* out, int mode, const double* denom) {
-        double* in = c->red;
-        double* nxt = c->red + c->red_cap / 2;
-        while (nrows > 1) {
-            const int64_t threads = nrows * bp;
-            const unsigned g = grid_for(threads, kBlock);
-            DG_TRY(launch(c, kNorms, 8.0 * threads, [&] {
-                DISPATCH_B1(bp, k_fold<BP><<<g, kBlock, 0, c->stream>>>(nrows, in, nxt));
-            }));
-            nrows = g;
-            std::swap(in, nxt);
-        }
-        DG_TRY(launch(c, kNorms, 0.0, [&] { k_finalize<<<1, 32, 0, c->stream>>>(nrhs, in, out, mode, denom); }));
-        return Status::Ok();
-    }
-
-    // out[lane] = ||b||_2 over level-0 rows of vector v (mode 1) or sum (0)
-    Status sumsq(const double* v, double* out, int mode) {
-        const int n = c->lv[0].nv;
-        DG_TRY(launch(c, kNorms, 8.0 * n * nrhs, [&] {
-            DISPATCH_BP(key, k_sumsq<BP, RPT><<<rows_grid(n), kBlock, 0, c->stream>>>(n, nrhs, v, c->red));
-        }));
-        return reduce_partials(partial_blocks(n), out, mode, nullptr);
-    }
-
-    // hist[lane] = ||b - A x||_2 / denom[lane] on level 0 (multigrid.cpp:317-319)
-    Status resnorm(double* hist, const double* denom) {
-        DG_TRY(ensure_x(0));
-        Level& L = c->lv[0];
-        const double* x = xcur(L);
-        const double bytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 16.0 * L.nv * nrhs;
-        if (L.Le_ci && tpr <= 8) {
-            int g = 0;
-            DG_TRY(PIPE_W(L.Le_w, OP_RES_NORM, kFineResidual, bytes, L.nv, L.Le_ci, L.Le_v, L.Le_row, x, b0,
-                          nullptr, c->red, nullptr, 0.0, &g));
-            return reduce_partials(g, hist, 2, denom);
-        }
-        DG_TRY(launch(c, kFineResidual, bytes, [&] {
-            DISPATCH_BP(key, (k_residual<BP, RPT, 0, false><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b0, nullptr, c->red)))
-        }));
-        return reduce_partials(partial_blocks(L.nv), hist, 2, denom);
-    }
-
-    // denom[lane] = ||b|| > 0 ? ||b|| : 1   (multigrid.cpp:307-308)
-    Status make_denom(double* denom) {
-        double* bn = c->dsmall + 64;
-        DG_TRY(sumsq(b0, bn, 1));
-        DG_TRY(launch(c, kNorms, 0.0, [&] { k_denom<<<1, 32, 0, c->stream>>>(nrhs, bn, denom); }));
-        return Status::Ok();
-    }
-
-    // Can the next cycle's first level-0 sweep carry the residual norm of the
-    // current iterate? (walk starts with a level-0 pre-smoothing on the
-    // pipelined path and x is materialized)
-    bool can_fuse(const Plan& plan) const {
-        const Level& L = c->lv[0];
-        return c->lv.size() > 1 && !plan.walk.empty() && plan.walk[0] == 'd' && plan.pre[0] >= 1 && !L.x_zero &&
-               L.Le_ci && tpr <= 8 && L.zero_diag_row < 0;
-    }
-
-    Status one_cycle(const Plan& plan) {
-        if (c->lv.size() == 1) return coarse_solve(0);
-        return cycle_once(plan);
-    }
-
-    Status load_x0(const double* d_x0) {
-        Level& L = c->lv[0];
-        if (d_x0) {
-            DG_CUDA(cudaMemcpyAsync(xcur(L), d_x0, sizeof(double) * L.nv * nrhs, cudaMemcpyDeviceToDevice,
-                                    c->stream));
-            L.x_zero = false;
-        } else {
-            L.x_zero = true;
-        }
-        return Status::Ok();
-    }
-};
-
-Status check_nrhs(const decmg_gpu_ctx* c, int nrhs) {
-    if (nrhs < 1 || nrhs > c->max_nrhs || nrhs > 32)
-        return Status::Err(DECMG_INVALID_ARGUMENT, "nrhs must be in [1, max_nrhs] (max 32)");
-    return Status::Ok();
-}
 
 }  // namespace
 

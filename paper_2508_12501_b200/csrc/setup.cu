@@ -692,7 +692,10 @@ Status assemble(decmg_gpu_ctx* c, Level& m, bool dirichlet) {
     return Status::Ok();
 }
 
-Status morton_order(decmg_gpu_ctx* c, Level& m) {
+}  // namespace
+
+// Bounding box of a level's positions and the 21-bit quantization scale.
+Status level_bbox(decmg_gpu_ctx* c, const Level& m, double lo[3], double sc[3]) {
     TmpPool tp(c->stream);
     unsigned long long* mm;
     DG_TRY(tp.get(&mm, 6));
@@ -702,7 +705,6 @@ Status morton_order(decmg_gpu_ctx* c, Level& m) {
     unsigned long long h[6];
     DG_CUDA(cudaMemcpyAsync(h, mm, sizeof h, cudaMemcpyDeviceToHost, c->stream));
     DG_CUDA(cudaStreamSynchronize(c->stream));
-    double lo[3], sc[3];
     for (int k = 0; k < 3; ++k) {
         auto dec = [](unsigned long long u) {
             u = (u >> 63) ? (u & 0x7fffffffffffffffULL) : ~u;
@@ -714,13 +716,33 @@ Status morton_order(decmg_gpu_ctx* c, Level& m) {
         const double ext = dec(h[3 + k]) - lo[k];
         sc[k] = ext > 0.0 ? 2097151.0 / ext : 0.0;
     }
+    return Status::Ok();
+}
+
+// Morton keys of a level's positions in a given box (ids written to d_id if non-null).
+Status morton_keys(decmg_gpu_ctx* c, const Level& m, const double lo[3], const double sc[3],
+                   unsigned long long* d_keys, int* d_id) {
+    TmpPool tp(c->stream);
+    int* id = d_id;
+    if (!id) DG_TRY(tp.get(&id, m.nv));
+    LAUNCH(4, m.nv, k_morton, m.nv, m.pos, lo[0], lo[1], lo[2], sc[0], sc[1], sc[2], d_keys, id);
+    DG_CUDA(cudaStreamSynchronize(c->stream));
+    return Status::Ok();
+}
+
+namespace {
+
+Status morton_order(decmg_gpu_ctx* c, Level& m) {
+    TmpPool tp(c->stream);
+    double lo[3], sc[3];
+    DG_TRY(level_bbox(c, m, lo, sc));
     unsigned long long *kin, *kout;
     int *iin;
     DG_TRY(tp.get(&kin, m.nv));
     DG_TRY(tp.get(&kout, m.nv));
     DG_TRY(tp.get(&iin, m.nv));
     DG_TRY(dalloc(c, &m.ord, m.nv));
-    LAUNCH(4, m.nv, k_morton, m.nv, m.pos, lo[0], lo[1], lo[2], sc[0], sc[1], sc[2], kin, iin);
+    DG_TRY(morton_keys(c, m, lo, sc, kin, iin));
     size_t bytes = 0;
     DG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, iin, m.ord, m.nv, 0, 64, c->stream));
     void* tmp;

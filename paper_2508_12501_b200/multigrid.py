@@ -412,3 +412,93 @@ def gmg_solve(h: MultigridHierarchy, plan: CyclePlan, b: np.ndarray, tol: float,
     return SolveReport(solution=x, residual_history=[hist[: done[j], j].tolist() for j in range(nrhs)],
                        cumulative_seconds=[], iterations=done.tolist(), converged=(final <= tol).tolist(),
                        final_relative_residual=final.tolist(), wall_seconds=wall)
+
+
+class DistributedHierarchy:
+    """Vertex-partitioned multi-GPU hierarchy.
+
+    world_size ranks; with nccl_id=None all ranks are emulated in this process
+    on one device (device copies instead of NCCL -- the parity tests), else
+    this process is `rank` of a one-process-per-GPU job and nccl_id is the
+    128-byte id from `nccl_unique_id()` on rank 0.
+    """
+
+    def __init__(self, base, nsub: int, world_size: int, rank: int = 0, nccl_id: Optional[bytes] = None,
+                 dirichlet: bool = False, project_sphere: Optional[bool] = None, device: int = 0, max_nrhs: int = 1,
+                 agglomerate_below: int = 65536):
+        self._lib = _lib.load()
+        if isinstance(base, str):
+            if project_sphere is None:
+                project_sphere = base == "ico"
+            pos, tri = base_mesh(base)
+        else:
+            pos, tri = base
+        pos = np.ascontiguousarray(pos, dtype=np.float64)
+        tri = np.ascontiguousarray(tri, dtype=np.int32)
+        flags = (_lib.DECMG_PROJECT_SPHERE if project_sphere else 0) | (_lib.DECMG_DIRICHLET if dirichlet else 0)
+        cfg = decmg_gpu_config(device=device, max_nrhs=max_nrhs)
+        out = C.c_void_p()
+        idbuf = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), len(nccl_id))
+        check(self._lib.decmg_gpu_dist_create(_ptr(pos), pos.shape[0], _ptr(tri), tri.shape[0], nsub, flags,
+                                              C.byref(cfg), world_size, rank, idbuf, agglomerate_below,
+                                              C.byref(out)), None, dist=True)
+        self._d = out
+        self.world_size = world_size
+        self.dirichlet = dirichlet
+        ka, lv, own, halo = C.c_int(), C.c_int(), C.c_int64(), C.c_int64()
+        self._lib.decmg_gpu_dist_info(self._d, C.byref(ka), C.byref(lv), C.byref(own), C.byref(halo))
+        self.agglomeration_level, self.nlevels = ka.value, lv.value
+        self.owned0, self.halo0 = own.value, halo.value
+
+    def close(self):
+        if getattr(self, "_d", None) and self._d.value:
+            self._lib.decmg_gpu_dist_destroy(self._d)
+            self._d = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def levels(self) -> int:
+        return self.nlevels
+
+    def _run(self, plan, b, x0, cycles, solve, tol):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        nrhs = 1 if b.ndim == 1 else b.shape[1]
+        ps, keep = _plan_struct(plan, self.nlevels)
+        if x0 is not None:
+            x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        x = np.empty_like(b)
+        hist = np.zeros((max(cycles, 1), nrhs))
+        done = np.zeros(nrhs, dtype=np.int32)
+        fin = np.zeros(nrhs)
+        check(self._lib.decmg_gpu_dist_run(self._d, C.byref(ps), nrhs, _ptr(b), None if x0 is None else _ptr(x0),
+                                           cycles, int(solve), tol, _ptr(x), _ptr(hist), _ptr(done), _ptr(fin)),
+              self._d, dist=True)
+        return x, hist, done, fin
+
+    def run_cycle(self, plan: CyclePlan, b, x0=None) -> CycleResult:
+        x, hist, done, fin = self._run(plan, b, x0, plan.cycles, False, 0.0)
+        hist = hist[: plan.cycles]
+        return CycleResult(x=x, residual_history=hist[:, 0] if np.ndim(b) == 1 else hist)
+
+    def gmg_solve(self, plan: CyclePlan, b, tol: float, max_cycles: int, x0=None) -> SolveReport:
+        t0 = time.perf_counter()
+        x, hist, done, fin = self._run(plan, b, x0, max_cycles, True, tol)
+        wall = time.perf_counter() - t0
+        if np.ndim(b) == 1:
+            it = int(done[0])
+            return SolveReport(solution=x, residual_history=hist[:it, 0].tolist(), cumulative_seconds=[],
+                               iterations=it, converged=bool(fin[0] <= tol), final_relative_residual=float(fin[0]),
+                               wall_seconds=wall)
+        return SolveReport(solution=x, residual_history=[hist[: done[j], j].tolist() for j in range(len(done))],
+                           cumulative_seconds=[], iterations=done.tolist(), converged=(fin <= tol).tolist(),
+                           final_relative_residual=fin.tolist(), wall_seconds=wall)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(_lib.load().decmg_gpu_nccl_unique_id(buf, 128))
+    return buf.raw
