@@ -11,10 +11,12 @@ as 16 x 10,485,762 unknowns).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun): every rank solves its own 16-RHS batch on its own GPU
-(weak scaling, no data-path collective; the elapsed time is the max over
-ranks). `--impl reference` times the reference's CPU solver (oracle/_ref,
-the reference compiled in place) on a bounded sample on the host cores.
+N > 1 (torchrun, one process per GPU): the same workload partitioned across
+the GPUs by vertex (Morton-key ranges, 1-ring halos exchanged with NCCL
+grouped send/recv, coarse levels replicated) -- strong
+scaling of the fixed problem; the cycle time is the max over ranks.
+`--impl reference` times the reference's CPU solver (oracle/_ref, the
+reference compiled in place) on a bounded sample on the host cores.
 """
 from __future__ import annotations
 
@@ -63,7 +65,8 @@ def max_over_ranks(world, v: float) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -74,9 +77,20 @@ def sum_over_ranks(world, v: float) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def share_nccl_id(world, rank, make_id):
+    """ncclUniqueId created on rank 0 and broadcast over torch.distributed."""
+    obj = [make_id() if rank == 0 else None]
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.broadcast_object_list(obj, src=0)
+    return obj[0]
 
 
 class ClockSampler:
@@ -287,6 +301,75 @@ def run_ours(args, world, rank, local):
         print(json.dumps(out), flush=True)
 
 
+# ------------------------------------------------------------ partitioned ----
+def run_partitioned(args, world, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_12501_b200 as d
+
+    torch.cuda.set_device(local)
+    uid = share_nccl_id(world, rank, d.nccl_unique_id)
+    t0 = time.perf_counter()
+    dh = d.DistributedHierarchy("ico", args.nsub, world, rank=rank, nccl_id=uid, device=local,
+                                max_nrhs=args.nrhs)
+    setup_s = time.perf_counter() - t0
+    g = dh.context()
+    n = g.n()
+    levels = dh.levels()
+    plan = d.standard_plan(levels, d.CycleKind.V, 2, 2)
+    B = g.make_rhs("uniform", SEED0, args.nrhs)  # the same batch as the 1-GPU run
+    Bp = g.project_compatible(B)
+    hb = torch.from_numpy(Bp).pin_memory().numpy()
+    # warm-up, then K steps (one run of K cycles); cycle-loop time by CUDA events in the library
+    plan.cycles = args.warmup
+    dh.run_cycle(plan, hb)
+    plan.cycles = args.steps
+    g.set_timing(True)
+    g.timing(-1)
+    launches0 = dh.launch_count()
+    with ClockSampler(local) as clk:
+        barrier(world)
+        res = dh.run_cycle(plan, hb)
+        barrier(world)
+    ms = max_over_ranks(world, dh.last_cycle_ms())
+    launches = dh.launch_count() - launches0
+    cls = {c: g.timing(c) for c in range(8)}
+    g.set_timing(False)
+    value = float(n) * args.nrhs * args.steps / (ms / 1e3)
+    nl, tms, tbytes = cls[0]
+    peak, peak_kind = measured_peak()
+    achieved = (tbytes / max(nl, 1)) / (tms / max(nl, 1) / 1e3) / 1e9 if nl else None
+    roofline = {"bound": "hbm", "kernel": "k_rowop_pipe<16,4,W,OP_SWEEP> (level-0 sweep, this rank's rows)",
+                "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": achieved / peak if achieved else None, "traffic": None,
+                "algorithmic_bytes_per_launch": tbytes / max(nl, 1), "launches": nl}
+    # e2e: gmg_solve to 1e-8 from pinned host memory to pinned host memory
+    hB = torch.from_numpy(B).pin_memory().numpy()
+    dh.gmg_solve(d.standard_plan(levels, d.CycleKind.V, 2, 2), hB, 1e-8, 200)
+    barrier(world)
+    t0 = time.perf_counter()
+    rep = dh.gmg_solve(d.standard_plan(levels, d.CycleKind.V, 2, 2), hB, 1e-8, 200)
+    e2e_s = max_over_ranks(world, time.perf_counter() - t0)
+    cyc = sum(rep.iterations)
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"BASELINE config 4: icosphere x{args.nsub} ({n} vertices, {levels} levels), "
+                                  f"{args.nrhs} RHS batch, weighted-Jacobi V(2,2), coarse CG, fp64, vertex-partitioned",
+                      "vertices": n, "levels": levels, "nrhs": args.nrhs, "global_batch": args.nrhs,
+                      "parallelism": f"vertex partition x{world} (Morton-key ranges, NCCL halo exchange, "
+                                     f"levels >= {dh.agglomeration_level} replicated)",
+                      "owned_rows_rank0": dh.owned0, "halo_rows_rank0": dh.halo0, "setup_s": setup_s,
+                      "l2": "vectors >> 126 MB L2", "last_step_rel_residual_max": float(np.max(res.residual_history[-1]))},
+           "roofline": roofline,
+           "e2e": {"value": float(n) * cyc / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(B.nbytes),
+                   "d2h_bytes_per_step": int(B.nbytes), "time_to_1e-8_s": e2e_s, "cycles_to_1e-8": rep.iterations},
+           "gpu_launches": int(launches), "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
 # ------------------------------------------------------------- reference ----
 def run_reference(args, world, rank):
     """The reference's own CPU solver (oracle/_ref/ref_harness: the reference
@@ -336,12 +419,16 @@ def main():
     ap.add_argument("--nrhs", type=int, default=NRHS)
     ap.add_argument("--ref-nsub", type=int, default=9)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="use the vertex-partitioned NCCL path even at N = 1 (plumbing check)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     world, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, world, rank)
+    elif world > 1 or args.partitioned:
+        run_partitioned(args, world, rank, local)
     else:
         run_ours(args, world, rank, local)
     if world > 1:

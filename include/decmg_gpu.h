@@ -186,6 +186,14 @@ DECMG_API int decmg_gpu_dist_info(const decmg_gpu_dist* d, int* agglomeration_le
 /* run_cycle (solve == 0, ncycles = max_cycles) or gmg_solve (solve != 0) with
  * full-length host vectors replicated on every rank; x_out receives the full
  * solution on every rank. */
+/* CUDA-event time of the last decmg_gpu_dist_run's cycle loop on this rank
+ * (cycles + per-cycle residual norms; excludes input staging, projection and
+ * the solution gather), and the kernel launches of this rank so far. */
+/* The full (replicated) hierarchy of this rank: every single-context entry
+ * point (make_rhs, export, apply, timing, ...) works on it; owned by d. */
+DECMG_API decmg_gpu_ctx* decmg_gpu_dist_context(decmg_gpu_dist* d);
+DECMG_API double decmg_gpu_dist_last_cycle_ms(const decmg_gpu_dist* d);
+DECMG_API int64_t decmg_gpu_dist_launch_count(const decmg_gpu_dist* d);
 DECMG_API int decmg_gpu_dist_run(decmg_gpu_dist* d, const decmg_gpu_plan* plan, int nrhs, const double* b,
                                  const double* x0, int max_cycles, int solve, double tol, double* x_out,
                                  double* hist_out, int* cycles_done, double* final_out);

@@ -88,6 +88,9 @@ SIGNATURES = {
     "decmg_gpu_dist_last_error": (C.c_char_p, [C.c_void_p]),
     "decmg_gpu_dist_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int64),
                                       C.POINTER(C.c_int64)]),
+    "decmg_gpu_dist_context": (C.c_void_p, [C.c_void_p]),
+    "decmg_gpu_dist_last_cycle_ms": (C.c_double, [C.c_void_p]),
+    "decmg_gpu_dist_launch_count": (C.c_int64, [C.c_void_p]),
     "decmg_gpu_dist_run": (C.c_int, [C.c_void_p, C.POINTER(decmg_gpu_plan), C.c_int, C.c_void_p, C.c_void_p,
                                      C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
 }

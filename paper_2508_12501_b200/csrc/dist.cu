@@ -131,6 +131,8 @@ struct decmg_gpu_dist {
     std::string err;
     std::vector<void*> allocs;
     double* hsum = nullptr;               // pinned [world][32]
+    float last_cycle_ms = 0.f;            // device time of the last run's cycle loop
+    cudaEvent_t ev[2] = {nullptr, nullptr};
 };
 
 namespace decmg_gpu {
@@ -723,6 +725,11 @@ Status dist_run(decmg_gpu_dist* D, const Plan& plan, int nrhs, const double* h_b
         }));
         return Status::Ok();
     };
+    if (!D->ev[0]) {
+        DG_CUDA(cudaEventCreate(&D->ev[0]));
+        DG_CUDA(cudaEventCreate(&D->ev[1]));
+    }
+    DG_CUDA(cudaEventRecord(D->ev[0], st));
     while (cyc < maxc && active) {
         DG_TRY(dd.cycle_once(plan));
         ++cyc;
@@ -740,6 +747,9 @@ Status dist_run(decmg_gpu_dist* D, const Plan& plan, int nrhs, const double* h_b
             active &= ~finm;
         }
     }
+    DG_CUDA(cudaEventRecord(D->ev[1], st));
+    DG_CUDA(cudaEventSynchronize(D->ev[1]));
+    DG_CUDA(cudaEventElapsedTime(&D->last_cycle_ms, D->ev[0], D->ev[1]));
     if (active) DG_TRY(snapshot(active));
     DG_CUDA(cudaMemcpyAsync(h_x, g->xsol, nb, cudaMemcpyDeviceToHost, st));
     DG_CUDA(cudaStreamSynchronize(st));
@@ -817,10 +827,18 @@ void decmg_gpu_dist_destroy(decmg_gpu_dist* D) {
     if (!D) return;
     if (D->g) cudaStreamSynchronize(D->g->stream);
     if (D->comm) ncclCommDestroy(D->comm);
+    for (cudaEvent_t e : D->ev)
+        if (e) cudaEventDestroy(e);
     for (void* p : D->allocs) cudaFree(p);
     if (D->hsum) cudaFreeHost(D->hsum);
     delete D;
 }
+
+decmg_gpu_ctx* decmg_gpu_dist_context(decmg_gpu_dist* D) { return D ? D->g.get() : nullptr; }
+
+double decmg_gpu_dist_last_cycle_ms(const decmg_gpu_dist* D) { return D ? D->last_cycle_ms : -1.0; }
+
+int64_t decmg_gpu_dist_launch_count(const decmg_gpu_dist* D) { return D && D->g ? D->g->launch_count : -1; }
 
 const char* decmg_gpu_dist_last_error(const decmg_gpu_dist* D) {
     return D ? D->err.c_str() : g_dist_create_error.c_str();

@@ -197,10 +197,11 @@ class MultigridHierarchy:
     _DT = {"positions": np.float64, "dual_areas": np.float64, "diag": np.float64, "L_values": np.float64,
            "P_values": np.float64, "R_values": np.float64}
 
-    def __init__(self, ctx: int, dirichlet: bool, max_nrhs: int):
+    def __init__(self, ctx: int, dirichlet: bool, max_nrhs: int, owned: bool = True):
         self._ctx = C.c_void_p(ctx)
         self.dirichlet = dirichlet
         self.max_nrhs = max_nrhs
+        self._owned = owned
         self._lib = _lib.load()
 
     # -- construction ------------------------------------------------------
@@ -269,9 +270,9 @@ class MultigridHierarchy:
         return cls(out.value, dirichlet, max_nrhs)
 
     def close(self) -> None:
-        if self._ctx and self._ctx.value:
+        if self._ctx and self._ctx.value and self._owned:
             self._lib.decmg_gpu_destroy(self._ctx)
-            self._ctx = C.c_void_p()
+        self._ctx = C.c_void_p()
 
     def __del__(self):
         try:
@@ -445,6 +446,7 @@ class DistributedHierarchy:
         self._d = out
         self.world_size = world_size
         self.dirichlet = dirichlet
+        self.max_nrhs = max_nrhs
         ka, lv, own, halo = C.c_int(), C.c_int(), C.c_int64(), C.c_int64()
         self._lib.decmg_gpu_dist_info(self._d, C.byref(ka), C.byref(lv), C.byref(own), C.byref(halo))
         self.agglomeration_level, self.nlevels = ka.value, lv.value
@@ -463,6 +465,17 @@ class DistributedHierarchy:
 
     def levels(self) -> int:
         return self.nlevels
+
+    def last_cycle_ms(self) -> float:
+        return self._lib.decmg_gpu_dist_last_cycle_ms(self._d)
+
+    def context(self) -> "MultigridHierarchy":
+        """Non-owning view of this rank's full (replicated) hierarchy."""
+        return MultigridHierarchy(self._lib.decmg_gpu_dist_context(self._d), self.dirichlet, self.max_nrhs,
+                                  owned=False)
+
+    def launch_count(self) -> int:
+        return self._lib.decmg_gpu_dist_launch_count(self._d)
 
     def _run(self, plan, b, x0, cycles, solve, tol):
         b = np.ascontiguousarray(b, dtype=np.float64)
