@@ -142,6 +142,7 @@ struct decmg_gpu_ctx {
     double* io_x = nullptr;
     int64_t launch_count = 0;
     int rpt = 4;
+    double wtot0 = 0.0;         // sum of level-0 dual areas in the reference order
     int num_sms = 148;                // right-hand sides per thread in the vector mapping (env DECMG_RPT)
     decmg_gpu::Timing timing;
     std::string err;

@@ -104,7 +104,7 @@ Status project_compatible(decmg_gpu_ctx* c, int nrhs, double* d_b) {
     const size_t smem = static_cast<size_t>(kProjStages) * kProjRows * (nrhs + 1) * sizeof(double);
     DG_CUDA(cudaFuncSetAttribute(k_project_sums, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     DG_TRY(launch(c, kNorms, 8.0 * L.nv * (nrhs + 1), [&] {
-        k_project_sums<<<1, 64, smem, c->stream>>>(L.nv, nrhs, L.area, d_b, mean);
+        k_project_sums<<<1, 64, smem, c->stream>>>(L.nv, nrhs, L.area, d_b, c->wtot0, mean);
     }));
     const unsigned g = grid_for(static_cast<int64_t>(L.nv) * bp, kBlock);
     DG_TRY(launch(c, kNorms, 16.0 * L.nv * nrhs, [&] {

@@ -797,6 +797,14 @@ Status build_ell(decmg_gpu_ctx* c, int nrows, const int* rp, const int* ci, cons
 // in the reference order), then the reordered L, P and R.
 Status build_orders(decmg_gpu_ctx* c) {
     const int L = static_cast<int>(c->lv.size());
+    {  // project_compatible's `total += w[i]` chain (multigrid.cpp:244-247), once
+        const Level& m = c->lv[0];
+        std::vector<double> a(m.nv);
+        DG_CUDA(cudaMemcpy(a.data(), m.area, sizeof(double) * m.nv, cudaMemcpyDeviceToHost));
+        double t = 0.0;
+        for (double x : a) t += x;
+        c->wtot0 = t;
+    }
     for (int k = 0; k + 1 < L; ++k)
         if (c->lv[k].pos) DG_TRY(morton_order(c, c->lv[k]));
     for (int k = 0; k < L; ++k) {
