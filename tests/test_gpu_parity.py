@@ -307,3 +307,69 @@ def test_config5_full_size(base, nsub, dirichlet, rhs):
     hist = np.array(rep.residual_history)
     assert np.all(hist[1:] < hist[:-1])
     np.testing.assert_allclose(hist[:2], oh, rtol=RTOL_HIST)
+
+
+@pytest.mark.parametrize("nrhs", [2, 3, 5, 32])
+def test_odd_batch_widths_bitwise(nrhs):
+    """Every thread mapping (scalar lanes for non-power-of-two batches, 2- and
+    4-wide vector lanes) gives each RHS its single-vector reference iterate."""
+    base, nsub = "ico", 4
+    h = d.MultigridHierarchy.from_base(base, nsub, max_nrhs=nrhs)
+    o = OracleHierarchy(base, nsub)
+    B = np.stack([o.project(o.rhs("uniform", 40 + j)) for j in range(nrhs)], axis=1)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan.cycles = 3
+    res = h.run_cycle(plan, B)
+    for j in range(nrhs):
+        ox, oh = o.run_cycles(B[:, j], ncycles=3)
+        np.testing.assert_array_equal(res.x[:, j], ox)
+        assert np.all(np.abs(res.residual_history[:, j] - oh) <= RTOL_HIST * oh)
+
+
+def test_warm_start_and_cycle_cap():
+    """x0 warm start (gmg_solve's optional x0, solvers.cpp:251-258), the cycle
+    cap (max_cycles hit: not converged) and max_cycles = 0 (the solution is x0)."""
+    base, nsub = "ico", 5
+    h = d.MultigridHierarchy.from_base(base, nsub)
+    o = OracleHierarchy(base, nsub)
+    b = o.rhs("uniform", 8)
+    x0 = np.random.default_rng(1).uniform(-1, 1, h.n())
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    bp = o.project(b)
+    plan.cycles = 3
+    res = h.run_cycle(plan, bp, x0)
+    ox, oh = o.run_cycles(bp, x0=x0, ncycles=3)
+    np.testing.assert_array_equal(res.x, ox)
+    rep = d.gmg_solve(h, plan, b, 1e-30, 4)
+    assert rep.iterations == 4 and not rep.converged
+    rep0 = d.gmg_solve(h, plan, b, 1e-8, 0, x0=x0)
+    assert rep0.iterations == 0
+    np.testing.assert_array_equal(rep0.solution, x0)
+
+
+def test_w_cycle_solve_and_one_level_solve():
+    """gmg_solve with a W-cycle plan and on a one-level hierarchy (the coarse
+    CG alone, multigrid.cpp:312-313)."""
+    h = d.MultigridHierarchy.from_base("equi:4:8:1.0", 3)
+    o = OracleHierarchy("equi:4:8:1.0", 3)
+    b = o.rhs("lr", 23)
+    plan = d.standard_plan(h.levels(), d.CycleKind.W, 2, 2)
+    rep = d.gmg_solve(h, plan, b, 1e-10, 50)
+    assert rep.converged
+    bp = o.project(b)
+    ox, oh = o.run_cycles(bp, ncycles=rep.iterations, walk=plan.walk_string())
+    np.testing.assert_array_equal(rep.solution, ox)
+    one = d.MultigridHierarchy.from_base("equi:4:8:1.0", 0)
+    rep1 = d.gmg_solve(one, d.standard_plan(1, d.CycleKind.V), one.make_rhs("lr", 5), 1e-12, 3)
+    assert rep1.iterations == 1 and rep1.final_relative_residual <= 1e-12
+
+
+def test_setup_errors_match_reference_messages():
+    """Non-well-centred dual cell (operators.cpp:88-98) and degenerate triangle
+    (geometry.cpp:11-13) raise runtime_error with the reference's message."""
+    P = np.array([[0, 0, 0], [1, 0, 0], [0.5, 0.1, 0], [0.5, -0.1, 0]], float)
+    with pytest.raises(RuntimeError, match="non-well-centered dual cell at vertex 0"):
+        d.MultigridHierarchy.from_base((P, np.array([[0, 1, 2], [0, 3, 1]])), 0)
+    Q = np.array([[0, 0, 0], [1, 0, 0], [2, 0, 0]], float)
+    with pytest.raises(RuntimeError, match="circumcenter: degenerate triangle"):
+        d.MultigridHierarchy.from_base((Q, np.array([[0, 1, 2]])), 0)
