@@ -65,7 +65,7 @@ Status run_cycles(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_
     DG_TRY(check_nrhs(c, nrhs));
     if (ncycles < 0) return Status::Err(DECMG_INVALID_ARGUMENT, "CyclePlan: negative cycle count");
     const double* b_in = d_b;
-    if ((reinterpret_cast<uintptr_t>(d_b) & 15) != 0) {  // vector loads need 16-byte alignment
+    if ((reinterpret_cast<uintptr_t>(d_b) & 31) != 0) {  // 256-bit vector loads need 32-byte alignment
         DG_CUDA(cudaMemcpyAsync(c->bproj, d_b, sizeof(double) * c->lv[0].nv * nrhs, cudaMemcpyDeviceToDevice,
                                 c->stream));
         b_in = c->bproj;
