@@ -143,7 +143,8 @@ struct decmg_gpu_ctx {
     int64_t launch_count = 0;
     int rpt = 4;
     double wtot0 = 0.0;         // sum of level-0 dual areas in the reference order
-    int num_sms = 148;                // right-hand sides per thread in the vector mapping (env DECMG_RPT)
+    int num_sms = 148;
+    int kmode = 1;              // row kernel: 1 high-occupancy ELL (default), 0 pipelined (env DECMG_KERNEL=pipe)                // right-hand sides per thread in the vector mapping (env DECMG_RPT)
     decmg_gpu::Timing timing;
     std::string err;
     std::vector<void*> allocations;

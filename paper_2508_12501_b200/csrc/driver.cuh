@@ -49,21 +49,28 @@ struct Driver {
                 int* grid = nullptr) {
         Status st;
         DISPATCH_BP(key, {
-            using G = PipeGeom<BP, RPT, W>;
-            static_assert((G::ROWS * 4 % 16 == 0 && G::CI_BYTES % 16 == 0) || BP / RPT > 8, "pipe tile");
-            const int ntiles = (nrows + G::ROWS - 1) / G::ROWS;
-            const int g = ntiles < 2 * c->num_sms ? ntiles : 2 * c->num_sms;
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(k_rowop_pipe<BP, RPT, W, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(G::SMEM));
-                attr = true;
+            PipeArgs a{0, nrhs, eci, ev, erow, x, b, out, partial, zr, omega};
+            if (c->kmode == 1) {  // high-occupancy ELL row kernel (default)
+                const unsigned g = grid_for(static_cast<int64_t>(nrows) * (BP / RPT), kBlock);
+                st = launch(c, cls, bytes, [&] { k_rowop_ell<BP, RPT, W, OP><<<g, kBlock, 0, c->stream>>>(a, nrows); });
+                if (grid) *grid = static_cast<int>(g);
+            } else {  // persistent pipelined kernel with the TMA-bulk index ring
+                using G = PipeGeom<BP, RPT, W>;
+                static_assert((G::ROWS * 4 % 16 == 0 && G::CI_BYTES % 16 == 0) || BP / RPT > 8, "pipe tile");
+                const int ntiles = (nrows + G::ROWS - 1) / G::ROWS;
+                const int g = ntiles < 2 * c->num_sms ? ntiles : 2 * c->num_sms;
+                static bool attr = false;
+                if (!attr) {
+                    cudaFuncSetAttribute(k_rowop_pipe<BP, RPT, W, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(G::SMEM));
+                    attr = true;
+                }
+                a.ntiles = ntiles;
+                st = launch(c, cls, bytes, [&] {
+                    k_rowop_pipe<BP, RPT, W, OP><<<g, kPipeThreads, G::SMEM, c->stream>>>(a);
+                });
+                if (grid) *grid = g;
             }
-            PipeArgs a{ntiles, nrhs, eci, ev, erow, x, b, out, partial, zr, omega};
-            st = launch(c, cls, bytes, [&] {
-                k_rowop_pipe<BP, RPT, W, OP><<<g, kPipeThreads, G::SMEM, c->stream>>>(a);
-            });
-            if (grid) *grid = g;
         })
         return st;
     }
