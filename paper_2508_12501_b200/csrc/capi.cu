@@ -36,7 +36,10 @@ Status init_ctx(decmg_gpu_ctx* c, const decmg_gpu_config* cfg) {
     DG_CUDA(cudaSetDevice(c->device));
     DG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     DG_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
-    if (const char* e = std::getenv("DECMG_KERNEL")) c->kmode = std::string(e) == "pipe" ? 0 : 1;
+    if (const char* e = std::getenv("DECMG_KERNEL")) {
+        const std::string m(e);
+        c->kmode = m == "pipe" ? 0 : (m == "ell" ? 1 : 2);
+    }
     if (const char* e = std::getenv("DECMG_RPT")) {
         const int v = std::atoi(e);
         if (v == 1 || v == 2 || v == 4) c->rpt = v;

@@ -144,7 +144,7 @@ struct decmg_gpu_ctx {
     int rpt = 4;
     double wtot0 = 0.0;         // sum of level-0 dual areas in the reference order
     int num_sms = 148;
-    int kmode = 1;              // row kernel: 1 high-occupancy ELL (default), 0 pipelined (env DECMG_KERNEL=pipe)                // right-hand sides per thread in the vector mapping (env DECMG_RPT)
+    int kmode = 2;              // row kernels: 2 auto (default), 0 pipelined, 1 high-occupancy (env DECMG_KERNEL)                // right-hand sides per thread in the vector mapping (env DECMG_RPT)
     decmg_gpu::Timing timing;
     std::string err;
     std::vector<void*> allocations;

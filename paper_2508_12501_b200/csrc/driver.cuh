@@ -50,7 +50,10 @@ struct Driver {
         Status st;
         DISPATCH_BP(key, {
             PipeArgs a{0, nrhs, eci, ev, erow, x, b, out, partial, zr, omega};
-            if (c->kmode == 1) {  // high-occupancy ELL row kernel (default)
+            // pipelined kernel for the 7/8-wide operators (L, R), the
+            // high-occupancy kernel for P (2-wide rows); env DECMG_KERNEL forces one
+            const bool ell = c->kmode == 1 || (c->kmode == 2 && W == 2);
+            if (ell) {
                 const unsigned g = grid_for(static_cast<int64_t>(nrows) * (BP / RPT), kBlock);
                 st = launch(c, cls, bytes, [&] { k_rowop_ell<BP, RPT, W, OP><<<g, kBlock, 0, c->stream>>>(a, nrows); });
                 if (grid) *grid = static_cast<int>(g);
