@@ -94,6 +94,13 @@ struct Level {
     int Le_w = 0;            // ELL widths (7 or 8; 0 = no ELL copy)
     int Re_w = 0;
     int* Le_row = nullptr;   // original row id per ELL row of Le/Pe (padded, -1 = padding)
+    // Fused sweep pairs (k_sweep2): tiles of kS2Rows consecutive ELL rows; for
+    // each tile the ELL rows of its 1-ring halo, and per ELL entry the slot of
+    // its column in the tile's shared-memory vector (tile rows, then halo).
+    int* S2_hptr = nullptr;  // [ntiles+1]
+    int* S2_halo = nullptr;  // ELL row indices of halo rows
+    int* S2_slot = nullptr;  // [npad * Le_w]
+    int S2_maxhalo = -1;     // -1: no tiles
     int* Re_row = nullptr;   // original coarse row id per ELL row of Re
     int zero_diag_row = -1;  // first row with L_ii == 0 (-1: none)
     double wtot = 0.0;       // sum of dual areas, sequential (coarse solve)
@@ -144,6 +151,7 @@ struct decmg_gpu_ctx {
     int rpt = 4;
     double wtot0 = 0.0;         // sum of level-0 dual areas in the reference order
     int num_sms = 148;
+    int sweep2 = 1;             // fuse smoothing sweeps in pairs (env DECMG_SWEEP2=0 disables)
     int kmode = 2;              // row kernels: 2 auto (default), 0 pipelined, 1 high-occupancy (env DECMG_KERNEL)                // right-hand sides per thread in the vector mapping (env DECMG_RPT)
     decmg_gpu::Timing timing;
     std::string err;

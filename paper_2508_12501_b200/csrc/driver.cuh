@@ -92,13 +92,71 @@ struct Driver {
         return Status::Ok();
     }
 
+    // Fused sweep pair on level k (k_sweep2); norm_out != nullptr: also the
+    // residual norm of the incoming x (level 0, fused cycle-residual).
+    Status sweep_pair(int k, const Plan& plan, double* norm_out) {
+        Level& L = c->lv[k];
+        const bool zero = L.x_zero;
+        const double R = nrhs;
+        const double bytes = zero ? 8.0 * L.nv + 12.0 * L.nnzL + 4.0 * L.nv + 16.0 * L.nv * R
+                                  : 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
+        const int ntiles = (L.nv + kS2Rows - 1) / kS2Rows;
+        const size_t smem = static_cast<size_t>(kS2Rows + L.S2_maxhalo) * nrhs * sizeof(double);
+        S2Args a{L.nv, nrhs, L.Le_ci, L.Le_v, L.Le_row, L.S2_slot, L.S2_hptr, L.S2_halo, L.diag, xcur(L), bptr(k),
+                 L.x[L.cur ^ 1], c->red, plan.omega};
+        const int cls = zero ? kZeroSweep : (k == 0 ? kFineSweep : kCoarseLevels);
+        Status st;
+        DISPATCH_BP(key, {
+            auto go = [&](auto kern) {
+                static bool attr = false;
+                if (!attr) {
+                    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                    attr = true;
+                }
+                st = launch(c, cls, bytes, [&] { kern<<<ntiles, kBlock, smem, c->stream>>>(a); });
+            };
+            if (L.Le_w == 7) {
+                if (zero) go(k_sweep2<BP, RPT, 7, true, false>);
+                else if (norm_out) go(k_sweep2<BP, RPT, 7, false, true>);
+                else go(k_sweep2<BP, RPT, 7, false, false>);
+            } else {
+                if (zero) go(k_sweep2<BP, RPT, 8, true, false>);
+                else if (norm_out) go(k_sweep2<BP, RPT, 8, false, true>);
+                else go(k_sweep2<BP, RPT, 8, false, false>);
+            }
+        })
+        DG_TRY(st);
+        if (norm_out) DG_TRY(reduce_partials(ntiles, norm_out, 2, fuse_denom));
+        L.cur ^= 1;
+        L.x_zero = false;
+        return Status::Ok();
+    }
+
     Status smooth(int k, int iters, const Plan& plan) {
         Level& L = c->lv[k];
         if (iters <= 0) return Status::Ok();
         if (L.zero_diag_row >= 0)
             return Status::Err(DECMG_RUNTIME, "jacobi: zero diagonal at row " + std::to_string(L.zero_diag_row));
         const double R = nrhs;
-        for (int it = 0; it < iters; ++it) {
+        for (int it = 0; it < iters;) {
+            const bool fuse_norm = k == 0 && it == 0 && fuse_hist && !L.x_zero;
+            if (iters - it >= 2 && L.S2_maxhalo >= 0 && tpr <= 8 && c->sweep2) {
+                DG_TRY(sweep_pair(k, plan, fuse_norm ? fuse_hist : nullptr));
+                it += 2;
+                if (fuse_norm) {
+                    fuse_hist = nullptr;
+                    if (fuse_hook) {
+                        bool stop = false;
+                        DG_TRY(fuse_hook(L.x[L.cur ^ 1], &stop));
+                        if (stop) {
+                            L.cur ^= 1;  // x_prev stays the current iterate
+                            stopped = true;
+                            return Status::Ok();
+                        }
+                    }
+                }
+                continue;
+            }
             double* xo = L.x[L.cur ^ 1];
             const double* b = bptr(k);
             if (L.x_zero) {
@@ -110,7 +168,7 @@ struct Driver {
             } else {
                 const double bytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
                 const double* x = xcur(L);
-                if (k == 0 && it == 0 && fuse_hist && L.Le_ci && tpr <= 8) {
+                if (fuse_norm && L.Le_ci && tpr <= 8) {
                     int g = 0;
                     DG_TRY(PIPE_W(L.Le_w, OP_SWEEP_NORM, kFineSweep, bytes, L.nv, L.Le_ci, L.Le_v, L.Le_row, x, b,
                                   xo, c->red, nullptr, plan.omega, &g));
@@ -118,6 +176,7 @@ struct Driver {
                     fuse_hist = nullptr;
                     L.cur ^= 1;
                     L.x_zero = false;
+                    ++it;
                     if (fuse_hook) {
                         bool stop = false;
                         DG_TRY(fuse_hook(L.x[L.cur ^ 1], &stop));
@@ -140,6 +199,7 @@ struct Driver {
             }
             L.cur ^= 1;
             L.x_zero = false;
+            ++it;
         }
         return Status::Ok();
     }

@@ -23,6 +23,7 @@ namespace decmg_gpu {
 namespace {
 
 constexpr int kBlock = 256;
+constexpr int kS2RowsHost = 128;  // == kS2Rows (rowkernels.cuh)
 
 // ---------------------------------------------------------------- Vec3 -----
 // proj/include/decmg/geometry.hpp:12-43, component formulas verbatim.
@@ -793,6 +794,55 @@ Status build_ell(decmg_gpu_ctx* c, int nrows, const int* rp, const int* ci, cons
     return Status::Ok();
 }
 
+// Tiles and halos for the fused sweep pairs (rowkernels.cuh k_sweep2).
+Status build_sweep2(decmg_gpu_ctx* c, Level& m) {
+    if (!m.Le_ci || !m.Le_row) return Status::Ok();
+    const int n = m.nv, W = m.Le_w, TR = kS2RowsHost;
+    const int npad = (n + 223) / 224 * 224;
+    std::vector<int> ci(static_cast<size_t>(npad) * W), rowid(npad);
+    DG_CUDA(cudaMemcpy(ci.data(), m.Le_ci, sizeof(int) * ci.size(), cudaMemcpyDeviceToHost));
+    DG_CUDA(cudaMemcpy(rowid.data(), m.Le_row, sizeof(int) * npad, cudaMemcpyDeviceToHost));
+    std::vector<int> pos_of(n, -1);
+    for (int q = 0; q < n; ++q) pos_of[rowid[q]] = q;
+    const int ntiles = (n + TR - 1) / TR;
+    std::vector<int> hptr(ntiles + 1, 0), halo, slot(static_cast<size_t>(npad) * W, -1);
+    std::vector<int> stamp(n, -1), hslot(n, -1);
+    int maxh = 0;
+    for (int t = 0; t < ntiles; ++t) {
+        const int t0 = t * TR, t1 = std::min(n, t0 + TR);
+        int nh = 0;
+        for (int q = t0; q < t1; ++q)
+            for (int j = 0; j < W; ++j) {
+                const int v = ci[static_cast<size_t>(q) * W + j];
+                if (v < 0) continue;
+                const int qq = pos_of[v];
+                int sl;
+                if (qq >= t0 && qq < t1) {
+                    sl = qq - t0;
+                } else {
+                    if (stamp[qq] != t) {
+                        stamp[qq] = t;
+                        hslot[qq] = TR + nh++;
+                        halo.push_back(qq);
+                    }
+                    sl = hslot[qq];
+                }
+                slot[static_cast<size_t>(q) * W + j] = sl;
+            }
+        hptr[t + 1] = hptr[t] + nh;
+        maxh = std::max(maxh, nh);
+    }
+    DG_TRY(dalloc(c, &m.S2_hptr, hptr.size()));
+    DG_TRY(dalloc(c, &m.S2_halo, halo.size()));
+    DG_TRY(dalloc(c, &m.S2_slot, slot.size()));
+    DG_CUDA(cudaMemcpy(m.S2_hptr, hptr.data(), sizeof(int) * hptr.size(), cudaMemcpyHostToDevice));
+    if (!halo.empty())
+        DG_CUDA(cudaMemcpy(m.S2_halo, halo.data(), sizeof(int) * halo.size(), cudaMemcpyHostToDevice));
+    DG_CUDA(cudaMemcpy(m.S2_slot, slot.data(), sizeof(int) * slot.size(), cudaMemcpyHostToDevice));
+    m.S2_maxhalo = maxh;
+    return Status::Ok();
+}
+
 // Row orders for every level except the coarsest (its CG runs sequentially
 // in the reference order), then the reordered L, P and R.
 Status build_orders(decmg_gpu_ctx* c) {
@@ -834,6 +884,7 @@ Status build_orders(decmg_gpu_ctx* c) {
         DG_TRY(build_ell(c, m.nv, m.Lo_rp, m.Lo_ci, m.Lo_v, m.ord, -8, &m.Le_ci, &m.Le_v, &m.Le_row, &m.Le_w));
         DG_TRY(build_ell(c, m.nv, m.Po_rp, m.Po_ci, m.Po_v, m.ord, 2, &m.Pe_ci, &m.Pe_v, nullptr));
         DG_TRY(build_ell(c, cm.nv, m.Ro_rp, m.Ro_ci, m.Ro_v, cm.ord, -8, &m.Re_ci, &m.Re_v, &m.Re_row, &m.Re_w));
+        DG_TRY(build_sweep2(c, m));
         if (m.Pe_ci && !m.Le_row) {  // P rows share L's row ids
             m.Pe_ci = nullptr;
             m.Pe_v = nullptr;
