@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 
+#include <cstdlib>
 #include <cstring>
 
 namespace decmg_gpu {
@@ -840,6 +841,11 @@ Status build_sweep2(decmg_gpu_ctx* c, Level& m) {
         DG_CUDA(cudaMemcpy(m.S2_halo, halo.data(), sizeof(int) * halo.size(), cudaMemcpyHostToDevice));
     DG_CUDA(cudaMemcpy(m.S2_slot, slot.data(), sizeof(int) * slot.size(), cudaMemcpyHostToDevice));
     m.S2_maxhalo = maxh;
+    // the fused pair keeps (tile + halo) rows x nrhs doubles in shared memory
+    if (static_cast<size_t>(TR + maxh) * c->max_nrhs * sizeof(double) > 200 * 1024) m.S2_maxhalo = -1;
+    if (std::getenv("DECMG_DEBUG"))
+        std::fprintf(stderr, "decmg: level nv=%d sweep-pair tiles=%d halo avg=%.1f max=%d%s\n", n, ntiles,
+                     static_cast<double>(halo.size()) / ntiles, maxh, m.S2_maxhalo < 0 ? " (disabled)" : "");
     return Status::Ok();
 }
 
