@@ -107,11 +107,12 @@ struct Driver {
         const int cls = zero ? kZeroSweep : (k == 0 ? kFineSweep : kCoarseLevels);
         Status st;
         DISPATCH_BP(key, {
-            auto go = [&](auto kern) {
-                static bool attr = false;
-                if (!attr) {
+            auto go = [&](void (*kern)(S2Args)) {
+                // opt in to > 48 KB of dynamic shared memory, once per kernel
+                static std::vector<const void*> done;
+                if (std::find(done.begin(), done.end(), reinterpret_cast<const void*>(kern)) == done.end()) {
                     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-                    attr = true;
+                    done.push_back(reinterpret_cast<const void*>(kern));
                 }
                 st = launch(c, cls, bytes, [&] { kern<<<ntiles, kBlock, smem, c->stream>>>(a); });
             };
