@@ -151,7 +151,7 @@ struct decmg_gpu_ctx {
     int rpt = 4;
     double wtot0 = 0.0;         // sum of level-0 dual areas in the reference order
     int num_sms = 148;
-    int sweep2 = 1;             // fuse smoothing sweeps in pairs (env DECMG_SWEEP2=0 disables)
+    int sweep2 = 0;             // fused sweep pairs, opt-in (env DECMG_SWEEP2=1; slower on B200)
     int kmode = 2;              // row kernels: 2 auto (default), 0 pipelined, 1 high-occupancy (env DECMG_KERNEL)                // right-hand sides per thread in the vector mapping (env DECMG_RPT)
     decmg_gpu::Timing timing;
     std::string err;
