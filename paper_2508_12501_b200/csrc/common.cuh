@@ -18,6 +18,10 @@
 
 namespace decmg_gpu {
 
+// Row ids of the padded ELL operators (Le_row / Re_row) carry the slot of
+// the row's diagonal entry in bits kRowBits..30; -1 marks a padding row.
+constexpr int kRowBits = 28;
+
 // Error propagation without exceptions across the ABI.
 struct Status {
     int code = DECMG_OK;
@@ -93,7 +97,7 @@ struct Level {
     double* Re_v = nullptr;
     int Le_w = 0;            // ELL widths (7 or 8; 0 = no ELL copy)
     int Re_w = 0;
-    int* Le_row = nullptr;   // original row id per ELL row of Le/Pe (padded, -1 = padding)
+    int* Le_row = nullptr;   // original row id | diag slot << kRowBits per ELL row of Le/Pe (-1 = padding)
     // Fused sweep pairs (k_sweep2): tiles of kS2Rows consecutive ELL rows; for
     // each tile the ELL rows of its 1-ring halo, and per ELL entry the slot of
     // its column in the tile's shared-memory vector (tile rows, then halo).
@@ -148,11 +152,11 @@ struct decmg_gpu_ctx {
     double* io_x0 = nullptr;
     double* io_x = nullptr;
     int64_t launch_count = 0;
-    int rpt = 4;
+    int rpt = 4;                // right-hand sides per thread in the vector mapping (env DECMG_RPT)
     double wtot0 = 0.0;         // sum of level-0 dual areas in the reference order
     int num_sms = 148;
     int sweep2 = 0;             // fused sweep pairs, opt-in (env DECMG_SWEEP2=1; slower on B200)
-    int kmode = 2;              // row kernels: 2 auto (default), 0 pipelined, 1 high-occupancy (env DECMG_KERNEL)                // right-hand sides per thread in the vector mapping (env DECMG_RPT)
+    int kmode = 2;              // row kernels: 2 auto (default), 0 pipelined, 1 high-occupancy (env DECMG_KERNEL)
     decmg_gpu::Timing timing;
     std::string err;
     std::vector<void*> allocations;

@@ -87,7 +87,7 @@ struct DLevel {
     int Lw = 0;
     int* Lci = nullptr;
     double* Lv = nullptr;
-    int* Lrow = nullptr;    // local row id (0..nown-1), -1 padding
+    int* Lrow = nullptr;    // local row id (0..nown-1) | diag slot << kRowBits, -1 padding
     double* diag = nullptr; // [nown]
     int* bd = nullptr;      // [nown] Dirichlet flags of the owned rows (extension x1)
     int nR = 0;             // owned rows of R_k (vertices of level k+1)
@@ -187,8 +187,11 @@ Status fetch_csr(const int* rp, const int* ci, const double* v, int nrows, int64
 
 // ELL of the given rows (global row ids, in order) with columns mapped by
 // colmap (-1 entries are a bug: every referenced column is owned or halo).
+// Same layout as setup.cu k_ell_fill: padding entries are a real column with
+// value 0.0 (the row's diagonal column for L, diag = true; its first column
+// otherwise) and the row id carries the diagonal slot above kRowBits.
 Status build_local_ell(decmg_gpu_dist* D, const HostCSR& A, const std::vector<int>& rows, const std::vector<int>& rowid,
-                       const std::vector<int>& colmap, int W, int** eci, double** ev, int** erow) {
+                       const std::vector<int>& colmap, int W, bool diag, int** eci, double** ev, int** erow) {
     const size_t npad = (rows.size() + 223) / 224 * 224;
     std::vector<int> ci(npad * W, -1), rid(npad, -1);
     std::vector<double> v(npad * W, 0.0);
@@ -196,13 +199,22 @@ Status build_local_ell(decmg_gpu_dist* D, const HostCSR& A, const std::vector<in
         const int g = rows[q];
         const int k0 = A.rp[g], len = A.rp[g + 1] - k0;
         if (len > W) return Status::Err(DECMG_RUNTIME, "dist: row longer than the ELL width");
+        if (rowid[q] >= (1 << kRowBits)) return Status::Err(DECMG_RUNTIME, "dist: row id beyond the ELL row-id bits");
+        int slot = 0, padc = -1;
         for (int j = 0; j < len; ++j) {
             const int lc = colmap[A.ci[k0 + j]];
             if (lc < 0) return Status::Err(DECMG_RUNTIME, "dist: column outside owned + halo");
             ci[q * W + j] = lc;
             v[q * W + j] = A.v[k0 + j];
+            if (A.ci[k0 + j] == g) {
+                slot = j;
+                if (diag) padc = lc;
+            }
+            if (!diag && j == 0) padc = lc;
         }
-        rid[q] = rowid[q];
+        if (padc < 0 && len > 0) padc = ci[q * W];
+        for (int j = len; j < W; ++j) ci[q * W + j] = padc < 0 ? 0 : padc;
+        rid[q] = rowid[q] | (diag ? slot << kRowBits : 0);
     }
     DG_TRY(upload(D, eci, ci));
     DG_TRY(upload(D, ev, v));
@@ -329,7 +341,7 @@ Status build_dist(decmg_gpu_dist* D, int agglomerate) {
             const int lm = maxlen(Lh[k]);
             d.Lw = lm <= 7 ? 7 : 8;
             if (lm > 8) return Status::Err(DECMG_RUNTIME, "dist: vertex valence above 7 is not supported");
-            DG_TRY(build_local_ell(D, Lh[k], own[k][p], lrow, g2l[k], d.Lw, &d.Lci, &d.Lv, &d.Lrow));
+            DG_TRY(build_local_ell(D, Lh[k], own[k][p], lrow, g2l[k], d.Lw, true, &d.Lci, &d.Lv, &d.Lrow));
             std::vector<double> dg(d.nown, 0.0);
             d.zero_diag_row = -1;
             for (int q = 0; q < d.nown; ++q) {
@@ -355,7 +367,7 @@ Status build_dist(decmg_gpu_dist* D, int agglomerate) {
             const int rm = maxlen(Rh[k]);
             d.Rw = rm <= 7 ? 7 : 8;
             if (rm > 8) return Status::Err(DECMG_RUNTIME, "dist: restriction row longer than 8");
-            DG_TRY(build_local_ell(D, Rh[k], own[k + 1][p], rrow, g2l[k], d.Rw, &d.Rci, &d.Rv, &d.Rrow));
+            DG_TRY(build_local_ell(D, Rh[k], own[k + 1][p], rrow, g2l[k], d.Rw, false, &d.Rci, &d.Rv, &d.Rrow));
             // P rows: owned level-k vertices, columns at level k+1
             std::vector<int> pmap;
             if (next_dist) {
@@ -367,7 +379,7 @@ Status build_dist(decmg_gpu_dist* D, int agglomerate) {
                 pmap.resize(g->lv[k + 1].nv);
                 std::iota(pmap.begin(), pmap.end(), 0);
             }
-            DG_TRY(build_local_ell(D, Ph[k], own[k][p], lrow, pmap, 2, &d.Pci, &d.Pv, nullptr));
+            DG_TRY(build_local_ell(D, Ph[k], own[k][p], lrow, pmap, 2, false, &d.Pci, &d.Pv, nullptr));
             // halo exchange plan of level k
             for (int q = 0; q < N; ++q) {
                 if (q == p) continue;

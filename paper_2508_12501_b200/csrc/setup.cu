@@ -513,17 +513,28 @@ __global__ void k_row_maxlen(int n, const int* __restrict__ rp, int* mx) {
 }
 
 // rows >= n are padding (column -1, row id -1) up to npad
+// Padded ELL copy of a CSR operator in row order ord. Padding entries hold a
+// real column with value 0.0 -- the row itself for L (diag), the row's first
+// column otherwise -- so the row kernels need no validity test: s + 0.0 * x
+// equals s bit for bit for finite x (s starts at +0.0 and is never -0.0).
+// erow[q] = original row id | (slot of the diagonal entry << kRowBits)
+// (common.cuh), -1 for padding rows past n.
 __global__ void k_ell_fill(int n, int npad, int W, const int* __restrict__ rp, const int* __restrict__ ci,
-                           const double* __restrict__ v, const int* __restrict__ ord, int* __restrict__ eci,
-                           double* __restrict__ ev, int* __restrict__ erow) {
+                           const double* __restrict__ v, const int* __restrict__ ord, bool diag,
+                           int* __restrict__ eci, double* __restrict__ ev, int* __restrict__ erow) {
     const int64_t q = gtid();
     if (q >= npad) return;
     const int k0 = q < n ? rp[q] : 0, len = q < n ? rp[q + 1] - k0 : 0;
+    const int row = q < n ? (ord ? ord[q] : static_cast<int>(q)) : -1;
+    const int padc = q >= n ? -1 : (diag ? row : (len > 0 ? ci[k0] : 0));
+    int slot = 0;
     for (int j = 0; j < W; ++j) {
-        eci[q * W + j] = j < len ? ci[k0 + j] : -1;
+        const int c = j < len ? ci[k0 + j] : padc;
+        eci[q * W + j] = c;
         ev[q * W + j] = j < len ? v[k0 + j] : 0.0;
+        if (diag && j < len && c == row) slot = j;
     }
-    if (erow) erow[q] = q < n ? (ord ? ord[q] : static_cast<int>(q)) : -1;
+    if (erow) erow[q] = q < n ? (row | (slot << kRowBits)) : -1;
 }
 
 // ------------------------------------------------------------ helpers ------
@@ -772,7 +783,8 @@ Status permute_rows(decmg_gpu_ctx* c, int nrows, const int* ord, const int* rp, 
 // rows padded to a multiple of 224 (the largest pipelined tile, cycle.cu).
 // W < 0: pick the narrowest of |W|-1 and |W| that fits (7 or 8); *wout = width used.
 Status build_ell(decmg_gpu_ctx* c, int nrows, const int* rp, const int* ci, const double* v, const int* ord, int W,
-                 int** eci, double** ev, int** erow, int* wout = nullptr) {
+                 bool diag, int** eci, double** ev, int** erow, int* wout = nullptr) {
+    if (nrows >= (1 << kRowBits)) return Status::Err(DECMG_INVALID_ARGUMENT, "level too large for the ELL row ids");
     TmpPool tp(c->stream);
     int* mx;
     DG_TRY(tp.get(&mx, 1));
@@ -791,7 +803,7 @@ Status build_ell(decmg_gpu_ctx* c, int nrows, const int* rp, const int* ci, cons
     DG_TRY(dalloc(c, eci, static_cast<size_t>(npad) * W));
     DG_TRY(dalloc(c, ev, static_cast<size_t>(npad) * W));
     if (erow) DG_TRY(dalloc(c, erow, npad));
-    LAUNCH(4, npad, k_ell_fill, nrows, npad, W, rp, ci, v, ord, *eci, *ev, erow ? *erow : nullptr);
+    LAUNCH(4, npad, k_ell_fill, nrows, npad, W, rp, ci, v, ord, diag, *eci, *ev, erow ? *erow : nullptr);
     return Status::Ok();
 }
 
@@ -804,7 +816,7 @@ Status build_sweep2(decmg_gpu_ctx* c, Level& m) {
     DG_CUDA(cudaMemcpy(ci.data(), m.Le_ci, sizeof(int) * ci.size(), cudaMemcpyDeviceToHost));
     DG_CUDA(cudaMemcpy(rowid.data(), m.Le_row, sizeof(int) * npad, cudaMemcpyDeviceToHost));
     std::vector<int> pos_of(n, -1);
-    for (int q = 0; q < n; ++q) pos_of[rowid[q]] = q;
+    for (int q = 0; q < n; ++q) pos_of[rowid[q] & ((1 << kRowBits) - 1)] = q;
     const int ntiles = (n + TR - 1) / TR;
     std::vector<int> hptr(ntiles + 1, 0), halo, slot(static_cast<size_t>(npad) * W, -1);
     std::vector<int> stamp(n, -1), hslot(n, -1);
@@ -887,9 +899,9 @@ Status build_orders(decmg_gpu_ctx* c) {
     for (int k = 0; k + 1 < L; ++k) {  // the coarsest level only runs the sequential CG
         Level& m = c->lv[k];
         const Level& cm = c->lv[k + 1];
-        DG_TRY(build_ell(c, m.nv, m.Lo_rp, m.Lo_ci, m.Lo_v, m.ord, -8, &m.Le_ci, &m.Le_v, &m.Le_row, &m.Le_w));
-        DG_TRY(build_ell(c, m.nv, m.Po_rp, m.Po_ci, m.Po_v, m.ord, 2, &m.Pe_ci, &m.Pe_v, nullptr));
-        DG_TRY(build_ell(c, cm.nv, m.Ro_rp, m.Ro_ci, m.Ro_v, cm.ord, -8, &m.Re_ci, &m.Re_v, &m.Re_row, &m.Re_w));
+        DG_TRY(build_ell(c, m.nv, m.Lo_rp, m.Lo_ci, m.Lo_v, m.ord, -8, true, &m.Le_ci, &m.Le_v, &m.Le_row, &m.Le_w));
+        DG_TRY(build_ell(c, m.nv, m.Po_rp, m.Po_ci, m.Po_v, m.ord, 2, false, &m.Pe_ci, &m.Pe_v, nullptr));
+        DG_TRY(build_ell(c, cm.nv, m.Ro_rp, m.Ro_ci, m.Ro_v, cm.ord, -8, false, &m.Re_ci, &m.Re_v, &m.Re_row, &m.Re_w));
         DG_TRY(build_sweep2(c, m));
         if (m.Pe_ci && !m.Le_row) {  // P rows share L's row ids
             m.Pe_ci = nullptr;
