@@ -139,7 +139,8 @@ DECMG_API int decmg_gpu_apply(decmg_gpu_ctx* ctx, int level, char op, const doub
 
 /* Structure export for parity. counts = {nv, ne, nt, nnz(L), nnz(P), nnz(R)}.
  * name: positions, edges, triangles, corners, dual_areas, boundary, diag,
- * L_row_ptr, L_col_idx, L_values, P_*, R_*. Returns the element count (query
+ * L_row_ptr, L_col_idx, L_values, P_*, R_*, order (the Morton row order of the
+ * level's ELL operators: row q is vertex order[q]). Returns the element count (query
  * with out = NULL) or -1. hash = EmbeddedComplex2D::hash (mesh.cpp:112-119). */
 DECMG_API int decmg_gpu_levels(const decmg_gpu_ctx* ctx);
 DECMG_API int decmg_gpu_level_info(decmg_gpu_ctx* ctx, int level, int64_t counts[6]);

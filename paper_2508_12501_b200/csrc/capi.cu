@@ -284,6 +284,7 @@ int64_t decmg_gpu_export(decmg_gpu_ctx* ctx, int level, const char* name, void* 
     else if (s == "dual_areas") pick(m.area, m.nv, 8);
     else if (s == "boundary") pick(m.bd, m.nv, 4);
     else if (s == "diag") pick(m.diag, m.nv, 8);
+    else if (s == "order") pick(m.ord, m.nv, 4);
     else if (s == "L_row_ptr") pick(m.L_rp, m.nv + 1, 4);
     else if (s == "L_col_idx") pick(m.L_ci, m.nnzL, 4);
     else if (s == "L_values") pick(m.L_v, m.nnzL, 8);

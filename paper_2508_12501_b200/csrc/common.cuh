@@ -72,23 +72,32 @@ struct Level {
     int* R_ci = nullptr;
     double* R_v = nullptr;
     int64_t nnzR = 0;
-    // Locality-ordered copies used by the hot kernels:
-    // row r of an *o array is row ord[r] of the reference-layout array, with
-    // its entries in the reference order, so every row sum is bit-identical;
-    // vectors keep the reference vertex numbering. ord == nullptr: identity.
-    int* ord = nullptr;      // [nv] Morton order of the vertex positions
+    // Internal numbering: the V-cycle stores every
+    // vector of a level in the Morton order of its vertex positions -- row q
+    // of x, b, r is vertex ord[q] -- so row passes stream their own rows and
+    // the x gathers stay local. The *o operators are the reference operators
+    // renumbered on both sides (row q = reference row ord[q], columns mapped
+    // through inv of the column level) with every row's entries kept in the
+    // reference order, so each row sum is bit-identical. ord == nullptr:
+    // identity (the coarsest level, hierarchies without positions). The API
+    // keeps the reference numbering; level-0 vectors are permuted at the
+    // boundary (driver.cuh to_internal / from_internal).
+    int* ord = nullptr;      // [nv] internal row -> vertex
+    int* inv = nullptr;      // [nv] vertex -> internal row
+    double* diag_i = nullptr;  // L_ii by internal row (== diag without ord)
+    int* bd_i = nullptr;       // boundary flag by internal row (== bd without ord)
     int* Lo_rp = nullptr;
     int* Lo_ci = nullptr;
     double* Lo_v = nullptr;
-    int* Po_rp = nullptr;    // fine rows of P in this level's order
+    int* Po_rp = nullptr;    // fine rows of P (internal), coarse columns (internal)
     int* Po_ci = nullptr;
     double* Po_v = nullptr;
-    int* Ro_rp = nullptr;    // coarse rows of R in the coarse level's order
+    int* Ro_rp = nullptr;    // coarse rows of R (internal), fine columns (internal)
     int* Ro_ci = nullptr;
     double* Ro_v = nullptr;
-    // Padded ELL copies of Lo (width 8), Po (width 2), Ro (width 8) used when
-    // every row fits (nullptr otherwise): row q at [q*W, q*W + W), padding
-    // column -1 after the real entries.
+    // Padded ELL copies of Lo (width 7/8), Po (width 2), Ro (width 7/8) used
+    // when every row fits (nullptr otherwise): row q at [q*W, q*W + W),
+    // padding entries (real column, value 0.0) after the real ones.
     int* Le_ci = nullptr;
     double* Le_v = nullptr;
     int* Pe_ci = nullptr;
@@ -97,7 +106,7 @@ struct Level {
     double* Re_v = nullptr;
     int Le_w = 0;            // ELL widths (7 or 8; 0 = no ELL copy)
     int Re_w = 0;
-    int* Le_row = nullptr;   // original row id | diag slot << kRowBits per ELL row of Le/Pe (-1 = padding)
+    int* Le_row = nullptr;   // row q | diag slot << kRowBits per ELL row of Le/Pe (-1 = padding)
     // Fused sweep pairs (k_sweep2): tiles of kS2Rows consecutive ELL rows; for
     // each tile the ELL rows of its 1-ring halo, and per ELL entry the slot of
     // its column in the tile's shared-memory vector (tile rows, then halo).
@@ -105,13 +114,13 @@ struct Level {
     int* S2_halo = nullptr;  // ELL row indices of halo rows
     int* S2_slot = nullptr;  // [npad * Le_w]
     int S2_maxhalo = -1;     // -1: no tiles
-    int* Re_row = nullptr;   // original coarse row id per ELL row of Re
+    int* Re_row = nullptr;   // coarse row q per ELL row of Re (-1 = padding)
     int zero_diag_row = -1;  // first row with L_ii == 0 (-1: none)
     double wtot = 0.0;       // sum of dual areas, sequential (coarse solve)
     // work vectors [nv][max_nrhs]
     double* x[2] = {nullptr, nullptr};
     int cur = 0;
-    double* b = nullptr;
+    double* b = nullptr;     // level 0: the RHS in the internal numbering (driver.cuh to_internal)
     bool x_zero = false;     // x[cur] known to be exactly +0.0 (fresh descent)
 };
 

@@ -64,14 +64,12 @@ Status run_cycles(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_
                   int ncycles, double* d_x, double* d_hist) {
     DG_TRY(check_nrhs(c, nrhs));
     if (ncycles < 0) return Status::Err(DECMG_INVALID_ARGUMENT, "CyclePlan: negative cycle count");
+    Level& L = c->lv[0];
     const double* b_in = d_b;
-    if ((reinterpret_cast<uintptr_t>(d_b) & 31) != 0) {  // 256-bit vector loads need 32-byte alignment
-        DG_CUDA(cudaMemcpyAsync(c->bproj, d_b, sizeof(double) * c->lv[0].nv * nrhs, cudaMemcpyDeviceToDevice,
-                                c->stream));
-        b_in = c->bproj;
-    }
+    if (L.ord || (reinterpret_cast<uintptr_t>(d_b) & 31) != 0) b_in = L.b;  // internal copy (32-byte aligned)
     Driver dr{c, nrhs, bp_of(nrhs), b_in};
     dr.init();
+    if (b_in != d_b) DG_TRY(dr.to_internal(d_b, L.b));
     double* denom = c->dsmall;
     DG_TRY(dr.load_x0(d_x0));
     DG_TRY(dr.make_denom(denom));
@@ -88,9 +86,7 @@ Status run_cycles(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_
         }
     }
     DG_TRY(dr.ensure_x(0));
-    Level& L = c->lv[0];
-    DG_CUDA(cudaMemcpyAsync(d_x, L.x[L.cur], sizeof(double) * L.nv * nrhs, cudaMemcpyDeviceToDevice, c->stream));
-    return Status::Ok();
+    return dr.from_internal(L.x[L.cur], d_x);
 }
 
 Status project_compatible(decmg_gpu_ctx* c, int nrhs, double* d_b) {
@@ -123,9 +119,10 @@ Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, co
     Level& L0 = c->lv[0];
     const size_t nbytes = sizeof(double) * L0.nv * nrhs;
     DG_CUDA(cudaMemcpyAsync(c->bproj, d_b, nbytes, cudaMemcpyDeviceToDevice, c->stream));
-    if (!c->dirichlet) DG_TRY(project_compatible(c, nrhs, c->bproj));
-    Driver dr{c, nrhs, bp_of(nrhs), c->bproj};
+    if (!c->dirichlet) DG_TRY(project_compatible(c, nrhs, c->bproj));  // in the reference numbering
+    Driver dr{c, nrhs, bp_of(nrhs), L0.ord ? L0.b : c->bproj};
     dr.init();
+    if (L0.ord) DG_TRY(dr.to_internal(c->bproj, L0.b));
     double* denom = c->dsmall;
     double* dres = c->dsmall + 256;
     DG_TRY(dr.load_x0(d_x0));
@@ -201,7 +198,7 @@ Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, co
             k_copy_lanes<<<grid_for(total, kBlock), kBlock, 0, c->stream>>>(total, nrhs, active, src, c->xsol);
         }));
     }
-    DG_CUDA(cudaMemcpyAsync(d_x, c->xsol, nbytes, cudaMemcpyDeviceToDevice, c->stream));
+    DG_TRY(dr.from_internal(c->xsol, d_x));
     DG_CUDA(cudaStreamSynchronize(c->stream));
     for (int l = 0; l < nrhs; ++l) {
         if (cycles_done) cycles_done[l] = done[l];

@@ -94,7 +94,7 @@ struct DLevel {
     int Rw = 0;
     int* Rci = nullptr;
     double* Rv = nullptr;
-    int* Rrow = nullptr;    // local id at level k+1 (or global id when k+1 is replicated)
+    int* Rrow = nullptr;    // local id at level k+1 (internal row of the shared level when k+1 is replicated)
     int* Pci = nullptr;     // owned fine rows of P_k, ELL-2; cols local at k+1 (or global)
     double* Pv = nullptr;
     int zero_diag_row = -1;
@@ -113,8 +113,6 @@ struct DRank {
     XPeer* gather_peers = nullptr;
     std::vector<XPeer> bpeers;   // all-gather plan of level ka (owned coarse entries)
     std::vector<XPeer> xpeers;   // all-gather plan of level 0 (solution)
-    int* d_own_ka = nullptr;     // global ids of owned level-ka vertices
-    int nown_ka = 0;
     double* red = nullptr;
     double* dsum = nullptr;      // per-rank partial sums [nrhs]
 };
@@ -284,6 +282,14 @@ Status build_dist(decmg_gpu_dist* D, int agglomerate) {
             std::iota(order[k].begin(), order[k].end(), 0);
         }
     }
+    // the replicated levels (>= ka) run on the shared hierarchy in its internal
+    // numbering (common.cuh Level::ord): global ids of level ka map through inv
+    std::vector<int> inv_ka(g->lv[ka].nv);
+    if (g->lv[ka].inv) {
+        DG_TRY(download(g->lv[ka].inv, g->lv[ka].nv, &inv_ka));
+    } else {
+        std::iota(inv_ka.begin(), inv_ka.end(), 0);
+    }
     // reference-layout operators of the distributed levels
     std::vector<HostCSR> Lh(ka), Rh(ka), Ph(ka);
     for (int k = 0; k < ka; ++k) {
@@ -360,7 +366,7 @@ Status build_dist(decmg_gpu_dist* D, int agglomerate) {
             // R rows: owned level-(k+1) vertices
             const bool next_dist = k + 1 < ka;
             std::vector<int> rrow;
-            for (int u : own[k + 1][p]) rrow.push_back(next_dist ? -2 : u);  // filled below when distributed
+            for (int u : own[k + 1][p]) rrow.push_back(next_dist ? -2 : inv_ka[u]);  // filled below when distributed
             d.nR = static_cast<int>(own[k + 1][p].size());
             if (next_dist)
                 for (int q = 0; q < d.nR; ++q) rrow[q] = q;  // owned rows come first in the local numbering
@@ -376,8 +382,7 @@ Status build_dist(decmg_gpu_dist* D, int agglomerate) {
                 for (int v : own[k + 1][p]) pmap[v] = i++;
                 for (int v : halo[k + 1][p]) pmap[v] = i++;
             } else {
-                pmap.resize(g->lv[k + 1].nv);
-                std::iota(pmap.begin(), pmap.end(), 0);
+                pmap = inv_ka;
             }
             DG_TRY(build_local_ell(D, Ph[k], own[k][p], lrow, pmap, 2, false, &d.Pci, &d.Pv, nullptr));
             // halo exchange plan of level k
@@ -407,15 +412,22 @@ Status build_dist(decmg_gpu_dist* D, int agglomerate) {
         }
         // all-gather plans: level ka (restricted RHS) and level 0 (solution),
         // global-id slots, owned entries to every other rank
+        // (slots: internal rows at level ka, reference ids at level 0)
         auto allgather_plan = [&](int k, std::vector<XPeer>* peers) -> Status {
+            auto slots = [&](int r) {
+                std::vector<int> v = own[k][r];
+                if (k == ka)
+                    for (int& u : v) u = inv_ka[u];
+                return v;
+            };
             for (int q = 0; q < N; ++q) {
                 if (q == p) continue;
                 XPeer x;
                 x.rank = q;
                 x.nsend = static_cast<int>(own[k][p].size());
                 x.nrecv = static_cast<int>(own[k][q].size());
-                DG_TRY(upload(D, &x.d_send, own[k][p]));
-                DG_TRY(upload(D, &x.d_recv, own[k][q]));
+                DG_TRY(upload(D, &x.d_send, slots(p)));
+                DG_TRY(upload(D, &x.d_recv, slots(q)));
                 DG_TRY(dmalloc(D, &x.sbuf, static_cast<size_t>(x.nsend) * D->max_nrhs));
                 DG_TRY(dmalloc(D, &x.rbuf, static_cast<size_t>(x.nrecv) * D->max_nrhs));
                 peers->push_back(x);
@@ -424,8 +436,6 @@ Status build_dist(decmg_gpu_dist* D, int agglomerate) {
         };
         DG_TRY(allgather_plan(ka, &R.bpeers));
         DG_TRY(allgather_plan(0, &R.xpeers));
-        R.nown_ka = static_cast<int>(own[ka][p].size());
-        DG_TRY(upload(D, &R.d_own_ka, own[ka][p]));
         DG_TRY(dmalloc(D, &R.red, g->red_cap + static_cast<size_t>(N) * 32));
         DG_TRY(dmalloc(D, &R.dsum, 64));
     }
@@ -564,7 +574,7 @@ struct DistDriver {
             DLevel& d = R.lv[k];
             double* out = next_dist ? R.lv[k + 1].b : g()->lv[k + 1].b;
             const int* zr = nullptr;
-            if (g()->dirichlet) zr = next_dist ? R.lv[k + 1].bd : g()->lv[k + 1].bd;
+            if (g()->dirichlet) zr = next_dist ? R.lv[k + 1].bd : g()->lv[k + 1].bd_i;
             DG_TRY(drv[i].pipe_w<OP_SPMV>(d.Rw, k == 0 ? 2 : 4, 0.0, d.nR, d.Rci, d.Rv, d.Rrow, d.r, nullptr, out,
                                  nullptr, zr, 0.0, nullptr));
         }

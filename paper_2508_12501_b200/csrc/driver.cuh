@@ -61,7 +61,7 @@ struct Driver {
                 using G = PipeGeom<BP, RPT, W>;
                 static_assert((G::ROWS * 4 % 16 == 0 && G::CI_BYTES % 16 == 0) || BP / RPT > 8, "pipe tile");
                 const int ntiles = (nrows + G::ROWS - 1) / G::ROWS;
-                const int g = ntiles < 2 * c->num_sms ? ntiles : 2 * c->num_sms;
+                const int g = ntiles < kPipeCtasPerSm * c->num_sms ? ntiles : kPipeCtasPerSm * c->num_sms;
                 static bool attr = false;
                 if (!attr) {
                     cudaFuncSetAttribute(k_rowop_pipe<BP, RPT, W, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -102,7 +102,7 @@ struct Driver {
                                   : 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
         const int ntiles = (L.nv + kS2Rows - 1) / kS2Rows;
         const size_t smem = static_cast<size_t>(kS2Rows + L.S2_maxhalo) * nrhs * sizeof(double);
-        S2Args a{L.nv, nrhs, L.Le_ci, L.Le_v, L.Le_row, L.S2_slot, L.S2_hptr, L.S2_halo, L.diag, xcur(L), bptr(k),
+        S2Args a{L.nv, nrhs, L.Le_ci, L.Le_v, L.Le_row, L.S2_slot, L.S2_hptr, L.S2_halo, L.diag_i, xcur(L), bptr(k),
                  L.x[L.cur ^ 1], c->red, plan.omega};
         const int cls = zero ? kZeroSweep : (k == 0 ? kFineSweep : kCoarseLevels);
         Status st;
@@ -164,7 +164,7 @@ struct Driver {
                 const double bytes = 8.0 * L.nv + 16.0 * L.nv * R;
                 DG_TRY(launch(c, kZeroSweep, bytes, [&] {
                     DISPATCH_BP(key, k_sweep_zero<BP, RPT><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                        L.nv, nrhs, L.diag, b, xo, plan.omega));
+                                        L.nv, nrhs, L.diag_i, b, xo, plan.omega));
                 }));
             } else {
                 const double bytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
@@ -194,7 +194,7 @@ struct Driver {
                 } else {
                     DG_TRY(launch(c, k == 0 ? kFineSweep : kCoarseLevels, bytes, [&] {
                         DISPATCH_BP(key, (k_sweep<BP, RPT, 0><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                            L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b, xo, plan.omega)))
+                                            L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, nullptr, x, b, xo, plan.omega)))
                     }));
                 }
             }
@@ -220,18 +220,18 @@ struct Driver {
         } else {
             DG_TRY(launch(c, k == 0 ? kFineResidual : kCoarseLevels, rbytes, [&] {
                 DISPATCH_BP(key, (k_residual<BP, RPT, 0, true><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                    L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b, c->r, nullptr)))
+                                    L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, nullptr, x, b, c->r, nullptr)))
             }));
         }
         const double tbytes = 12.0 * L.nnzR + 4.0 * (C.nv + 1) + 8.0 * L.nv * R + 8.0 * C.nv * R;
-        const int* zr = c->dirichlet ? C.bd : nullptr;
+        const int* zr = c->dirichlet ? C.bd_i : nullptr;
         if (L.Re_ci && tpr <= 8) {
             DG_TRY(PIPE_W(L.Re_w, OP_SPMV, k == 0 ? kRestrict : kCoarseLevels, tbytes, C.nv, L.Re_ci, L.Re_v,
                           L.Re_row, c->r, nullptr, C.b, nullptr, zr, 0.0, nullptr));
         } else {
             DG_TRY(launch(c, k == 0 ? kRestrict : kCoarseLevels, tbytes, [&] {
                 DISPATCH_BP(key, (k_spmv<BP, RPT, 0><<<rows_grid(C.nv), kBlock, 0, c->stream>>>(
-                                    C.nv, nrhs, L.Ro_rp, L.Ro_ci, L.Ro_v, C.ord, c->r, C.b, zr)))
+                                    C.nv, nrhs, L.Ro_rp, L.Ro_ci, L.Ro_v, nullptr, c->r, C.b, zr)))
             }));
         }
         return Status::Ok();
@@ -253,7 +253,7 @@ struct Driver {
         } else {
             DG_TRY(launch(c, k == 0 ? kProlong : kCoarseLevels, bytes, [&] {
                 DISPATCH_BP(key, (k_prolong_add<BP, RPT, 0><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                    L.nv, nrhs, L.Po_rp, L.Po_ci, L.Po_v, L.ord, xc, xf)))
+                                    L.nv, nrhs, L.Po_rp, L.Po_ci, L.Po_v, nullptr, xc, xf)))
             }));
         }
         return Status::Ok();
@@ -340,7 +340,7 @@ struct Driver {
         }
         DG_TRY(launch(c, kFineResidual, bytes, [&] {
             DISPATCH_BP(key, (k_residual<BP, RPT, 0, false><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
-                                L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, L.ord, x, b0, nullptr, c->red)))
+                                L.nv, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, nullptr, x, b0, nullptr, c->red)))
         }));
         return reduce_partials(partial_blocks(L.nv), hist, 2, denom);
     }
@@ -367,11 +367,35 @@ struct Driver {
         return cycle_once(plan);
     }
 
+    // Level-0 vectors between the reference numbering (API) and the internal
+    // one (common.cuh Level::ord): dst[q] = src[ord[q]] / dst[ord[q]] = src[q].
+    Status to_internal(const double* src, double* dst) {
+        const Level& L = c->lv[0];
+        const int64_t t = static_cast<int64_t>(L.nv) * nrhs;
+        if (!L.ord) {
+            DG_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * t, cudaMemcpyDeviceToDevice, c->stream));
+            return Status::Ok();
+        }
+        return launch(c, kNorms, 16.0 * t, [&] {
+            k_permute<false><<<grid_for(t, kBlock), kBlock, 0, c->stream>>>(L.nv, nrhs, L.ord, src, dst);
+        });
+    }
+    Status from_internal(const double* src, double* dst) {
+        const Level& L = c->lv[0];
+        const int64_t t = static_cast<int64_t>(L.nv) * nrhs;
+        if (!L.ord) {
+            DG_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * t, cudaMemcpyDeviceToDevice, c->stream));
+            return Status::Ok();
+        }
+        return launch(c, kNorms, 16.0 * t, [&] {
+            k_permute<true><<<grid_for(t, kBlock), kBlock, 0, c->stream>>>(L.nv, nrhs, L.ord, src, dst);
+        });
+    }
+
     Status load_x0(const double* d_x0) {
         Level& L = c->lv[0];
         if (d_x0) {
-            DG_CUDA(cudaMemcpyAsync(xcur(L), d_x0, sizeof(double) * L.nv * nrhs, cudaMemcpyDeviceToDevice,
-                                    c->stream));
+            DG_TRY(to_internal(d_x0, xcur(L)));
             L.x_zero = false;
         } else {
             L.x_zero = true;

@@ -486,24 +486,38 @@ __global__ void k_morton(int n, const double* __restrict__ pos, double lx, doubl
     id[i] = static_cast<int>(i);
 }
 
+// Renumbering of a CSR operator: row r of the output is row ord[r] of the
+// input (ord == nullptr: identity) with its entries in the input order and
+// every column c replaced by cinv[c] (cinv == nullptr: unchanged).
 __global__ void k_perm_count(int n, const int* __restrict__ ord, const int* __restrict__ rp, int* cnt) {
     const int64_t r = gtid();
     if (r >= n) return;
-    const int o = ord[r];
+    const int o = ord ? ord[r] : static_cast<int>(r);
     cnt[r] = rp[o + 1] - rp[o];
 }
 
-__global__ void k_perm_fill(int n, const int* __restrict__ ord, const int* __restrict__ rp,
-                            const int* __restrict__ ci, const double* __restrict__ v,
+__global__ void k_perm_fill(int n, const int* __restrict__ ord, const int* __restrict__ cinv,
+                            const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ v,
                             const int* __restrict__ orp, int* __restrict__ oci, double* __restrict__ ov) {
     const int64_t r = gtid();
     if (r >= n) return;
-    const int o = ord[r];
+    const int o = ord ? ord[r] : static_cast<int>(r);
     const int src = rp[o], len = rp[o + 1] - src, dst = orp[r];
     for (int k = 0; k < len; ++k) {
-        oci[dst + k] = ci[src + k];
+        oci[dst + k] = cinv ? cinv[ci[src + k]] : ci[src + k];
         ov[dst + k] = v[src + k];
     }
+}
+
+__global__ void k_invert(int n, const int* __restrict__ ord, int* __restrict__ inv) {
+    const int64_t q = gtid();
+    if (q < n) inv[ord[q]] = static_cast<int>(q);
+}
+
+template <class T>
+__global__ void k_take(int n, const int* __restrict__ ord, const T* __restrict__ in, T* __restrict__ out) {
+    const int64_t q = gtid();
+    if (q < n) out[q] = in[ord[q]];
 }
 
 __global__ void k_row_maxlen(int n, const int* __restrict__ rp, int* mx) {
@@ -761,11 +775,19 @@ Status morton_order(decmg_gpu_ctx* c, Level& m) {
     void* tmp;
     DG_TRY(tp.get(reinterpret_cast<char**>(&tmp), bytes));
     DG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, iin, m.ord, m.nv, 0, 64, c->stream));
+    DG_TRY(dalloc(c, &m.inv, m.nv));
+    LAUNCH(4, m.nv, k_invert, m.nv, m.ord, m.inv);
     return Status::Ok();
 }
 
-Status permute_rows(decmg_gpu_ctx* c, int nrows, const int* ord, const int* rp, const int* ci, const double* v,
-                    int64_t nnz, int** orp, int** oci, double** ov) {
+Status permute_rows(decmg_gpu_ctx* c, int nrows, const int* ord, const int* cinv, const int* rp, const int* ci,
+                    const double* v, int64_t nnz, int** orp, int** oci, double** ov) {
+    if (!ord && !cinv) {  // identity on both sides: share the reference arrays
+        *orp = const_cast<int*>(rp);
+        *oci = const_cast<int*>(ci);
+        *ov = const_cast<double*>(v);
+        return Status::Ok();
+    }
     TmpPool tp(c->stream);
     int* cnt;
     DG_TRY(tp.get(&cnt, nrows + 1));
@@ -775,7 +797,7 @@ Status permute_rows(decmg_gpu_ctx* c, int nrows, const int* ord, const int* rp, 
     DG_TRY(dalloc(c, ov, nnz));
     LAUNCH(4, nrows, k_perm_count, nrows, ord, rp, cnt);
     DG_TRY(exclusive_scan(c, cnt, *orp, nrows));
-    LAUNCH(4, nrows, k_perm_fill, nrows, ord, rp, ci, v, *orp, *oci, *ov);
+    LAUNCH(4, nrows, k_perm_fill, nrows, ord, cinv, rp, ci, v, *orp, *oci, *ov);
     return Status::Ok();
 }
 
@@ -861,8 +883,9 @@ Status build_sweep2(decmg_gpu_ctx* c, Level& m) {
     return Status::Ok();
 }
 
-// Row orders for every level except the coarsest (its CG runs sequentially
-// in the reference order), then the reordered L, P and R.
+// Internal numbering for every level except the coarsest (its CG runs
+// sequentially in the reference order): Morton order, the renumbered L, P, R
+// (common.cuh Level), their ELL copies, diag and boundary flags by internal row.
 Status build_orders(decmg_gpu_ctx* c) {
     const int L = static_cast<int>(c->lv.size());
     {  // project_compatible's `total += w[i]` chain (multigrid.cpp:244-247), once
@@ -877,31 +900,31 @@ Status build_orders(decmg_gpu_ctx* c) {
         if (c->lv[k].pos) DG_TRY(morton_order(c, c->lv[k]));
     for (int k = 0; k < L; ++k) {
         Level& m = c->lv[k];
+        DG_TRY(permute_rows(c, m.nv, m.ord, m.inv, m.L_rp, m.L_ci, m.L_v, m.nnzL, &m.Lo_rp, &m.Lo_ci, &m.Lo_v));
         if (m.ord) {
-            DG_TRY(permute_rows(c, m.nv, m.ord, m.L_rp, m.L_ci, m.L_v, m.nnzL, &m.Lo_rp, &m.Lo_ci, &m.Lo_v));
+            DG_TRY(dalloc(c, &m.diag_i, m.nv));
+            LAUNCH(4, m.nv, k_take<double>, m.nv, m.ord, m.diag, m.diag_i);
+            if (m.bd) {
+                DG_TRY(dalloc(c, &m.bd_i, m.nv));
+                LAUNCH(4, m.nv, k_take<int>, m.nv, m.ord, m.bd, m.bd_i);
+            }
         } else {
-            m.Lo_rp = m.L_rp; m.Lo_ci = m.L_ci; m.Lo_v = m.L_v;
+            m.diag_i = m.diag;
+            m.bd_i = m.bd;
         }
         if (k + 1 < L) {
-            if (m.ord) {
-                DG_TRY(permute_rows(c, m.nv, m.ord, m.P_rp, m.P_ci, m.P_v, m.nnzP, &m.Po_rp, &m.Po_ci, &m.Po_v));
-            } else {
-                m.Po_rp = m.P_rp; m.Po_ci = m.P_ci; m.Po_v = m.P_v;
-            }
             const Level& cm = c->lv[k + 1];
-            if (cm.ord) {
-                DG_TRY(permute_rows(c, cm.nv, cm.ord, m.R_rp, m.R_ci, m.R_v, m.nnzR, &m.Ro_rp, &m.Ro_ci, &m.Ro_v));
-            } else {
-                m.Ro_rp = m.R_rp; m.Ro_ci = m.R_ci; m.Ro_v = m.R_v;
-            }
+            DG_TRY(permute_rows(c, m.nv, m.ord, cm.inv, m.P_rp, m.P_ci, m.P_v, m.nnzP, &m.Po_rp, &m.Po_ci, &m.Po_v));
+            DG_TRY(permute_rows(c, cm.nv, cm.ord, m.inv, m.R_rp, m.R_ci, m.R_v, m.nnzR, &m.Ro_rp, &m.Ro_ci, &m.Ro_v));
         }
     }
     for (int k = 0; k + 1 < L; ++k) {  // the coarsest level only runs the sequential CG
         Level& m = c->lv[k];
         const Level& cm = c->lv[k + 1];
-        DG_TRY(build_ell(c, m.nv, m.Lo_rp, m.Lo_ci, m.Lo_v, m.ord, -8, true, &m.Le_ci, &m.Le_v, &m.Le_row, &m.Le_w));
-        DG_TRY(build_ell(c, m.nv, m.Po_rp, m.Po_ci, m.Po_v, m.ord, 2, false, &m.Pe_ci, &m.Pe_v, nullptr));
-        DG_TRY(build_ell(c, cm.nv, m.Ro_rp, m.Ro_ci, m.Ro_v, cm.ord, -8, false, &m.Re_ci, &m.Re_v, &m.Re_row, &m.Re_w));
+        DG_TRY(build_ell(c, m.nv, m.Lo_rp, m.Lo_ci, m.Lo_v, nullptr, -8, true, &m.Le_ci, &m.Le_v, &m.Le_row, &m.Le_w));
+        DG_TRY(build_ell(c, m.nv, m.Po_rp, m.Po_ci, m.Po_v, nullptr, 2, false, &m.Pe_ci, &m.Pe_v, nullptr));
+        DG_TRY(build_ell(c, cm.nv, m.Ro_rp, m.Ro_ci, m.Ro_v, nullptr, -8, false, &m.Re_ci, &m.Re_v, &m.Re_row,
+                         &m.Re_w));
         DG_TRY(build_sweep2(c, m));
         if (m.Pe_ci && !m.Le_row) {  // P rows share L's row ids
             m.Pe_ci = nullptr;
