@@ -37,6 +37,8 @@ Status init_ctx(decmg_gpu_ctx* c, const decmg_gpu_config* cfg) {
     DG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     DG_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
     if (const char* e = std::getenv("DECMG_SWEEP2")) c->sweep2 = std::atoi(e) != 0;
+    if (const char* e = std::getenv("DECMG_PF")) c->pf = std::atoi(e);
+    if (const char* e = std::getenv("DECMG_PFL")) c->pfl = std::atoi(e);
     if (const char* e = std::getenv("DECMG_KERNEL")) {
         const std::string m(e);
         c->kmode = m == "pipe" ? 0 : (m == "ell" ? 1 : 2);

@@ -165,6 +165,8 @@ struct decmg_gpu_ctx {
     double wtot0 = 0.0;         // sum of level-0 dual areas in the reference order
     int num_sms = 148;
     int sweep2 = 0;             // fused sweep pairs, opt-in (env DECMG_SWEEP2=1; slower on B200)
+    int pf = 56;                // row-kernel prefetch distance in rows, 0 = off (env DECMG_PF)
+    int pfl = 2;                // prefetch into L1 (1) or L2 (2) (env DECMG_PFL)
     int kmode = 2;              // row kernels: 2 auto (default), 0 pipelined, 1 high-occupancy (env DECMG_KERNEL)
     decmg_gpu::Timing timing;
     std::string err;

@@ -49,7 +49,7 @@ struct Driver {
                 int* grid = nullptr) {
         Status st;
         DISPATCH_BP(key, {
-            PipeArgs a{0, nrhs, eci, ev, erow, x, b, out, partial, zr, omega};
+            PipeArgs a{0, nrhs, eci, ev, erow, x, b, out, partial, zr, omega, nrows, c->pf, c->pfl};
             // pipelined kernel for the 7/8-wide operators (L, R), the
             // high-occupancy kernel for P (2-wide rows); env DECMG_KERNEL forces one
             const bool ell = c->kmode == 1 || (c->kmode == 2 && W == 2);
