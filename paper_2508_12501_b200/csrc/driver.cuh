@@ -376,8 +376,12 @@ struct Driver {
             DG_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * t, cudaMemcpyDeviceToDevice, c->stream));
             return Status::Ok();
         }
+        const bool v4 = nrhs % 4 == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 31) == 0;
         return launch(c, kNorms, 16.0 * t, [&] {
-            k_permute<false><<<grid_for(t, kBlock), kBlock, 0, c->stream>>>(L.nv, nrhs, L.ord, src, dst);
+            if (v4)
+                k_permute4<false><<<grid_for(t / 4, kBlock), kBlock, 0, c->stream>>>(L.nv, nrhs, L.ord, src, dst);
+            else
+                k_permute<false><<<grid_for(t, kBlock), kBlock, 0, c->stream>>>(L.nv, nrhs, L.ord, src, dst);
         });
     }
     Status from_internal(const double* src, double* dst) {
@@ -387,8 +391,12 @@ struct Driver {
             DG_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * t, cudaMemcpyDeviceToDevice, c->stream));
             return Status::Ok();
         }
+        const bool v4 = nrhs % 4 == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 31) == 0;
         return launch(c, kNorms, 16.0 * t, [&] {
-            k_permute<true><<<grid_for(t, kBlock), kBlock, 0, c->stream>>>(L.nv, nrhs, L.ord, src, dst);
+            if (v4)
+                k_permute4<true><<<grid_for(t / 4, kBlock), kBlock, 0, c->stream>>>(L.nv, nrhs, L.ord, src, dst);
+            else
+                k_permute<true><<<grid_for(t, kBlock), kBlock, 0, c->stream>>>(L.nv, nrhs, L.ord, src, dst);
         });
     }
 
