@@ -167,6 +167,7 @@ struct decmg_gpu_ctx {
     int sweep2 = 0;             // fused sweep pairs, opt-in (env DECMG_SWEEP2=1; slower on B200)
     int pf = 56;                // row-kernel prefetch distance in rows, 0 = off (env DECMG_PF)
     int pfl = 2;                // prefetch into L1 (1) or L2 (2) (env DECMG_PFL)
+    int fuse_rr = 0;            // residual recomputed inside the restriction, opt-in (env DECMG_FUSE_RR=1; slower)
     int kmode = 2;              // row kernels: 2 auto (default), 0 pipelined, 1 high-occupancy (env DECMG_KERNEL)
     decmg_gpu::Timing timing;
     std::string err;

@@ -7,6 +7,7 @@
 
 #include <functional>
 #include <string>
+#include <type_traits>
 
 namespace decmg_gpu {
 namespace {
@@ -43,16 +44,22 @@ struct Driver {
 
     // Launch the pipelined persistent row kernel on an ELL operator.
     // Returns the grid size in *grid (the number of norm partials for OP_RES_NORM).
-    template <int OP, int W>
+    template <int OP, int W, int W2 = 0>
     Status pipe(int cls, double bytes, int nrows, const int* eci, const double* ev, const int* erow,
                 const double* x, const double* b, double* out, double* partial, const int* zr, double omega,
-                int* grid = nullptr) {
+                int* grid = nullptr, const PipeArgs* fine = nullptr) {
         Status st;
         DISPATCH_BP(key, {
             PipeArgs a{0, nrhs, eci, ev, erow, x, b, out, partial, zr, omega, nrows, c->pf, c->pfl};
+            if (fine) {  // OP_RESTRICT_RES: the fine level's L and right-hand side
+                a.fci = fine->fci;
+                a.fv = fine->fv;
+                a.fb = fine->fb;
+                a.n = fine->n;
+            }
             // pipelined kernel for the 7/8-wide operators (L, R), the
             // high-occupancy kernel for P (2-wide rows); env DECMG_KERNEL forces one
-            const bool ell = c->kmode == 1 || (c->kmode == 2 && W == 2);
+            const bool ell = OP != OP_RESTRICT_RES && (c->kmode == 1 || (c->kmode == 2 && W == 2));
             if (ell) {
                 const unsigned g = grid_for(static_cast<int64_t>(nrows) * (BP / RPT), kBlock);
                 st = launch(c, cls, bytes, [&] { k_rowop_ell<BP, RPT, W, OP><<<g, kBlock, 0, c->stream>>>(a, nrows); });
@@ -61,16 +68,17 @@ struct Driver {
                 using G = PipeGeom<BP, RPT, W>;
                 static_assert((G::ROWS * 4 % 16 == 0 && G::CI_BYTES % 16 == 0) || BP / RPT > 8, "pipe tile");
                 const int ntiles = (nrows + G::ROWS - 1) / G::ROWS;
-                const int g = ntiles < kPipeCtasPerSm * c->num_sms ? ntiles : kPipeCtasPerSm * c->num_sms;
+                const int per_sm = OP == OP_RESTRICT_RES ? 2 : kPipeCtasPerSm;
+                const int g = ntiles < per_sm * c->num_sms ? ntiles : per_sm * c->num_sms;
                 static bool attr = false;
                 if (!attr) {
-                    cudaFuncSetAttribute(k_rowop_pipe<BP, RPT, W, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(G::SMEM));
+                    cudaFuncSetAttribute(k_rowop_pipe<BP, RPT, W, OP, W2>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(G::SMEM));
                     attr = true;
                 }
                 a.ntiles = ntiles;
                 st = launch(c, cls, bytes, [&] {
-                    k_rowop_pipe<BP, RPT, W, OP><<<g, kPipeThreads, G::SMEM, c->stream>>>(a);
+                    k_rowop_pipe<BP, RPT, W, OP, W2><<<g, kPipeThreads, G::SMEM, c->stream>>>(a);
                 });
                 if (grid) *grid = g;
             }
@@ -213,6 +221,26 @@ struct Driver {
         const double R = nrhs;
         const double* x = xcur(L);
         const double* b = bptr(k);
+        if (c->fuse_rr && L.Le_ci && L.Re_ci && tpr <= 8) {
+            // one pass: every R row recomputes the fine residuals it needs
+            const double bytes = 12.0 * L.nnzR + 4.0 * (C.nv + 1) + 12.0 * L.nnzL + 4.0 * (L.nv + 1) +
+                                 16.0 * L.nv * R + 8.0 * C.nv * R;
+            PipeArgs fine{};
+            fine.fci = L.Le_ci;
+            fine.fv = L.Le_v;
+            fine.fb = b;
+            fine.n = L.nv;
+            const int* zr = c->dirichlet ? C.bd_i : nullptr;
+            const int cls = k == 0 ? kRestrict : kCoarseLevels;
+            auto go = [&](auto wr, auto wl) {
+                return pipe<OP_RESTRICT_RES, decltype(wr)::value, decltype(wl)::value>(
+                    cls, bytes, C.nv, L.Re_ci, L.Re_v, L.Re_row, x, nullptr, C.b, nullptr, zr, 0.0, nullptr, &fine);
+            };
+            using I7 = std::integral_constant<int, 7>;
+            using I8 = std::integral_constant<int, 8>;
+            if (L.Re_w == 7) return L.Le_w == 7 ? go(I7{}, I7{}) : go(I7{}, I8{});
+            return L.Le_w == 7 ? go(I8{}, I7{}) : go(I8{}, I8{});
+        }
         const double rbytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
         if (L.Le_ci && tpr <= 8) {
             DG_TRY(PIPE_W(L.Le_w, OP_RES_STORE, k == 0 ? kFineResidual : kCoarseLevels, rbytes, L.nv, L.Le_ci,
