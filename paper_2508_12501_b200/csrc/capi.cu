@@ -63,6 +63,8 @@ void destroy_ctx(decmg_gpu_ctx* c) {
     for (void* p : c->allocations) cudaFree(p);
     if (c->hsmall) cudaFreeHost(c->hsmall);
     if (c->hist_dev) cudaFree(c->hist_dev);
+    for (cudaEvent_t e : c->io_events) cudaEventDestroy(e);
+    if (c->io_stream) cudaStreamDestroy(c->io_stream);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -211,11 +213,12 @@ int decmg_gpu_solve(decmg_gpu_ctx* ctx, const decmg_gpu_plan* plan, int nrhs, co
     if (nrhs < 1 || nrhs > ctx->max_nrhs)
         return fail(ctx, Status::Err(DECMG_INVALID_ARGUMENT, "nrhs must be in [1, max_nrhs]"));
     const size_t n = static_cast<size_t>(ctx->lv[0].nv) * nrhs;
-    API_TRY(ctx, cuda_status(cudaMemcpyAsync(ctx->io_b, b, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D b"));
+    // H2D of b overlapped with the projection chain (stage_rhs), into ctx->bproj
+    API_TRY(ctx, stage_rhs(ctx, nrhs, b, !ctx->dirichlet));
     if (x0)
         API_TRY(ctx, cuda_status(cudaMemcpyAsync(ctx->io_x0, x0, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D x0"));
-    API_TRY(ctx, solve(ctx, p, nrhs, ctx->io_b, x0 ? ctx->io_x0 : nullptr, tol, max_cycles, ctx->io_x, hist_out,
-                       cycles_done, final_out));
+    API_TRY(ctx, solve(ctx, p, nrhs, nullptr, x0 ? ctx->io_x0 : nullptr, tol, max_cycles, ctx->io_x, hist_out,
+                       cycles_done, final_out, true));
     if (x_out)
         API_TRY(ctx, cuda_status(cudaMemcpyAsync(x_out, ctx->io_x, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H x"));
     API_TRY(ctx, cuda_status(cudaStreamSynchronize(ctx->stream), "gmg_solve"));

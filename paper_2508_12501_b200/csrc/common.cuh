@@ -160,6 +160,8 @@ struct decmg_gpu_ctx {
     double* io_b = nullptr;     // staging for host-pointer calls [n0][max_nrhs]
     double* io_x0 = nullptr;
     double* io_x = nullptr;
+    cudaStream_t io_stream = nullptr;        // chunked host copies (stage_rhs)
+    std::vector<cudaEvent_t> io_events;
     int64_t launch_count = 0;
     int rpt = 4;                // right-hand sides per thread in the vector mapping (env DECMG_RPT)
     double wtot0 = 0.0;         // sum of level-0 dual areas in the reference order
@@ -228,7 +230,8 @@ Status run_cycles(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_
                   const double* d_x0, int ncycles, double* d_x, double* d_hist);
 Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, const double* d_x0,
              double tol, int max_cycles, double* d_x, double* h_hist, int* cycles_done,
-             double* h_final);
+             double* h_final, bool staged = false);
+Status stage_rhs(decmg_gpu_ctx* c, int nrhs, const double* h_b, bool project);
 Status project_compatible(decmg_gpu_ctx* c, int nrhs, double* d_b);
 Status apply_op(decmg_gpu_ctx* c, int level, char op, const double* d_x, double* d_y);
 

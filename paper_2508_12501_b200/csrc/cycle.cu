@@ -89,37 +89,104 @@ Status run_cycles(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_
     return dr.from_internal(L.x[L.cur], d_x);
 }
 
+namespace {
+
+// The projection's mean chain over rows [r0, r1) (state in c->dsmall + 160),
+// mean_out on the last range.
+Status project_chain(decmg_gpu_ctx* c, int nrhs, const double* d_b, int r0, int r1, double* mean_out) {
+    const Level& L = c->lv[0];
+    double* state = c->dsmall + 160;
+    const size_t smem = static_cast<size_t>(kProjStages) * proj_rows(nrhs) * nrhs * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        DG_CUDA(cudaFuncSetAttribute(k_project_sums, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kProjStages * kProjTileBytes));
+        attr = true;
+    }
+    double* prod = c->r;  // scratch [n0][max_nrhs]: the residual buffer is free outside a cycle
+    const int64_t t = static_cast<int64_t>(r1 - r0) * nrhs;
+    DG_TRY(launch(c, kNorms, 8.0 * (r1 - r0) + 16.0 * t, [&] {
+        if (t > 0) k_project_products<<<grid_for(t, kBlock), kBlock, 0, c->stream>>>(r0, r1, nrhs, L.area, d_b, prod);
+    }));
+    return launch(c, kNorms, 8.0 * t, [&] {
+        k_project_sums<<<1, 64, smem, c->stream>>>(r0, r1, nrhs, prod, c->wtot0, state, mean_out);
+    });
+}
+
+Status project_subtract(decmg_gpu_ctx* c, int nrhs, const double* mean, double* d_b) {
+    const Level& L = c->lv[0];
+    const int bp = bp_of(nrhs);
+    const unsigned g = grid_for(static_cast<int64_t>(L.nv) * bp, kBlock);
+    return launch(c, kNorms, 16.0 * L.nv * nrhs, [&] {
+        DISPATCH_B1(bp, k_project<BP><<<g, kBlock, 0, c->stream>>>(L.nv, nrhs, mean, d_b));
+    });
+}
+
+}  // namespace
+
 Status project_compatible(decmg_gpu_ctx* c, int nrhs, double* d_b) {
     DG_TRY(check_nrhs(c, nrhs));
-    const int bp = bp_of(nrhs);
-    const Level& L = c->lv[0];
-    double* mean = c->dsmall + 128;
     // TMA bulk copies need 16-byte aligned sources (cudaMalloc'd buffers are)
     if ((reinterpret_cast<uintptr_t>(d_b) & 15) != 0)
         return Status::Err(DECMG_INVALID_ARGUMENT, "project_compatible: rhs must be 16-byte aligned");
-    const size_t smem = static_cast<size_t>(kProjStages) * kProjRows * (nrhs + 1) * sizeof(double);
-    DG_CUDA(cudaFuncSetAttribute(k_project_sums, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    DG_TRY(launch(c, kNorms, 8.0 * L.nv * (nrhs + 1), [&] {
-        k_project_sums<<<1, 64, smem, c->stream>>>(L.nv, nrhs, L.area, d_b, c->wtot0, mean);
-    }));
-    const unsigned g = grid_for(static_cast<int64_t>(L.nv) * bp, kBlock);
-    DG_TRY(launch(c, kNorms, 16.0 * L.nv * nrhs, [&] {
-        DISPATCH_B1(bp, k_project<BP><<<g, kBlock, 0, c->stream>>>(L.nv, nrhs, mean, d_b));
-    }));
-    return Status::Ok();
+    double* mean = c->dsmall + 128;
+    DG_CUDA(cudaMemsetAsync(c->dsmall + 160, 0, sizeof(double) * 32, c->stream));
+    DG_TRY(project_chain(c, nrhs, d_b, 0, c->lv[0].nv, mean));
+    return project_subtract(c, nrhs, mean, d_b);
+}
+
+// Host right-hand side -> c->bproj, projected (Neumann): the H2D copy runs in
+// chunks on a second stream and the sequential mean chain follows chunk by
+// chunk on the context stream, so the copy hides under the chain.
+Status stage_rhs(decmg_gpu_ctx* c, int nrhs, const double* h_b, bool project) {
+    DG_TRY(check_nrhs(c, nrhs));
+    const int n = c->lv[0].nv;
+    double* dst = c->bproj;
+    if (!project) {
+        DG_CUDA(cudaMemcpyAsync(dst, h_b, sizeof(double) * n * nrhs, cudaMemcpyHostToDevice, c->stream));
+        return Status::Ok();
+    }
+    if (!c->io_stream) DG_CUDA(cudaStreamCreateWithFlags(&c->io_stream, cudaStreamNonBlocking));
+    constexpr int kChunks = 16;
+    while (static_cast<int>(c->io_events.size()) < kChunks + 1) {
+        cudaEvent_t e;
+        DG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->io_events.push_back(e);
+    }
+    // the copy stream starts after everything already queued on the context stream
+    DG_CUDA(cudaEventRecord(c->io_events[kChunks], c->stream));
+    DG_CUDA(cudaStreamWaitEvent(c->io_stream, c->io_events[kChunks], 0));
+    int per = (n + kChunks - 1) / kChunks;
+    per = (per + proj_rows(nrhs) - 1) / proj_rows(nrhs) * proj_rows(nrhs);
+    DG_CUDA(cudaMemsetAsync(c->dsmall + 160, 0, sizeof(double) * 32, c->stream));
+    double* mean = c->dsmall + 128;
+    for (int k = 0; k < kChunks; ++k) {
+        const int r0 = std::min(n, k * per), r1 = std::min(n, r0 + per);
+        if (r1 > r0) {
+            const size_t off = static_cast<size_t>(r0) * nrhs;
+            DG_CUDA(cudaMemcpyAsync(dst + off, h_b + off, sizeof(double) * (r1 - r0) * nrhs, cudaMemcpyHostToDevice,
+                                    c->io_stream));
+        }
+        DG_CUDA(cudaEventRecord(c->io_events[k], c->io_stream));
+        DG_CUDA(cudaStreamWaitEvent(c->stream, c->io_events[k], 0));
+        if (r1 > r0 || k == kChunks - 1) DG_TRY(project_chain(c, nrhs, dst, r0, r1, k == kChunks - 1 ? mean : nullptr));
+    }
+    return project_subtract(c, nrhs, mean, dst);
 }
 
 // gmg_solve (proj/src/solvers.cpp:251-279), batched: each RHS stops at its
 // own cycle count; its solution is the iterate of that cycle.
 Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, const double* d_x0,
              double tol, int max_cycles, double* d_x, double* h_hist, int* cycles_done,
-             double* h_final) {
+             double* h_final, bool staged) {
     DG_TRY(check_nrhs(c, nrhs));
     if (max_cycles < 0) return Status::Err(DECMG_INVALID_ARGUMENT, "gmg_solve: max_cycles >= 0");
     Level& L0 = c->lv[0];
-    const size_t nbytes = sizeof(double) * L0.nv * nrhs;
-    DG_CUDA(cudaMemcpyAsync(c->bproj, d_b, nbytes, cudaMemcpyDeviceToDevice, c->stream));
-    if (!c->dirichlet) DG_TRY(project_compatible(c, nrhs, c->bproj));  // in the reference numbering
+    if (!staged) {  // staged: stage_rhs already left the projected RHS in c->bproj
+        const size_t nbytes = sizeof(double) * L0.nv * nrhs;
+        DG_CUDA(cudaMemcpyAsync(c->bproj, d_b, nbytes, cudaMemcpyDeviceToDevice, c->stream));
+        if (!c->dirichlet) DG_TRY(project_compatible(c, nrhs, c->bproj));  // in the reference numbering
+    }
     Driver dr{c, nrhs, bp_of(nrhs), L0.ord ? L0.b : c->bproj};
     dr.init();
     if (L0.ord) DG_TRY(dr.to_internal(c->bproj, L0.b));

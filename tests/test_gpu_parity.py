@@ -373,3 +373,29 @@ def test_setup_errors_match_reference_messages():
     Q = np.array([[0, 0, 0], [1, 0, 0], [2, 0, 0]], float)
     with pytest.raises(RuntimeError, match="circumcenter: degenerate triangle"):
         d.MultigridHierarchy.from_base((Q, np.array([[0, 1, 2]])), 0)
+
+
+@pytest.mark.parametrize("env", [{"DECMG_FUSE_RR": "1"}, {"DECMG_KERNEL": "ell"}, {"DECMG_SWEEP2": "1"},
+                                 {"DECMG_PF": "0"}, {"DECMG_RPT": "2"}])
+@pytest.mark.parametrize("base,nsub,dirichlet,nrhs", [("ico", 6, False, 16), ("square", 6, True, 1)])
+def test_kernel_variants_bitwise(monkeypatch, env, base, nsub, dirichlet, nrhs):
+    """Every opt-in kernel variant (fused residual-restriction, high-occupancy
+    row kernel, fused sweep pairs, no prefetch, 2 RHS per thread) gives the
+    reference iterate bit for bit. The switches are read at context creation."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    h = d.MultigridHierarchy.from_base(base, nsub, dirichlet=dirichlet, max_nrhs=nrhs)
+    o = OracleHierarchy(base, nsub, dirichlet)
+    if nrhs == 1:
+        B = o.rhs("sinsin" if dirichlet else "uniform", 5)[:, None]
+    else:
+        B = h.make_rhs("uniform", 40, nrhs)
+    if not dirichlet:
+        B = np.stack([o.project(B[:, j]) for j in range(nrhs)], axis=1)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan.cycles = 3
+    res = h.run_cycle(plan, B if nrhs > 1 else B[:, 0])
+    x = res.x if nrhs > 1 else res.x[:, None]
+    for j in range(nrhs):
+        ox, oh = o.run_cycles(B[:, j], ncycles=3)
+        np.testing.assert_array_equal(x[:, j], ox)
