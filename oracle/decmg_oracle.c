@@ -677,9 +677,12 @@ static int jacobi_sweep(const level_t* lv, double* x, const double* b, double om
     return 0;
 }
 
-/* gauss_seidel_sweep forward (proj/src/multigrid.cpp:13-34) */
-static int gs_sweep(const level_t* lv, double* x, const double* b) {
-    for (int i = 0; i < lv->m.nv; ++i) {
+/* gauss_seidel_sweep (proj/src/multigrid.cpp:13-34): rows in increasing
+ * order (reverse = 0) or decreasing order (reverse = 1), updated in place */
+static int gs_sweep(const level_t* lv, double* x, const double* b, int reverse) {
+    const int n = lv->m.nv;
+    for (int step = 0; step < n; ++step) {
+        const int i = reverse ? n - 1 - step : step;
         double diag = 0.0, sum = 0.0;
         for (int k = lv->L_rp[i]; k < lv->L_rp[i + 1]; ++k) {
             if (lv->L_ci[k] == i) diag = lv->L_v[k];
@@ -693,9 +696,17 @@ static int gs_sweep(const level_t* lv, double* x, const double* b) {
 
 typedef struct { int pre, post, smoother; double omega; } plan_t;
 
+/* smooth (proj/src/multigrid.cpp:95-120): 0 weighted Jacobi, 1 Gauss-Seidel,
+ * 2 symmetric Gauss-Seidel (forward then reverse per iteration) */
 static int smooth(const level_t* lv, double* x, const double* b, const plan_t* p, int iters, double* s) {
     for (int it = 0; it < iters; ++it) {
-        int rc = p->smoother == 0 ? jacobi_sweep(lv, x, b, p->omega, s) : gs_sweep(lv, x, b);
+        int rc;
+        if (p->smoother == 0) {
+            rc = jacobi_sweep(lv, x, b, p->omega, s);
+        } else {
+            rc = gs_sweep(lv, x, b, 0);
+            if (!rc && p->smoother == 2) rc = gs_sweep(lv, x, b, 1);
+        }
         if (rc) return rc;
     }
     return 0;

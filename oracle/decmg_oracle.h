@@ -48,7 +48,8 @@ void orc_spmv(const orc_hier* h, int k, const char* op, const double* x, double*
 double orc_norm2(const double* a, int64_t n);                  /* kernels::norm2 */
 uint64_t orc_fnv(const void* data, int64_t nbytes);
 
-/* smoother: 0 = weighted Jacobi (omega), 1 = Gauss-Seidel (forward).
+/* smoother: 0 = weighted Jacobi (omega), 1 = Gauss-Seidel (forward),
+ * 2 = symmetric Gauss-Seidel (forward + reverse per iteration).
  * walk: string of 'd'/'u' (NULL = V-cycle); pre/post sweeps uniform. */
 int orc_run_cycles(const orc_hier* h, const char* walk, int pre, int post, int smoother,
                    double omega, const double* b, const double* x0, int ncycles,

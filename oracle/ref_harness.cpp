@@ -383,13 +383,18 @@ int cmd_structure(const Case& c, int k, bool dirichlet, bool full) {
 
 SmootherConfig jacobi() { return SmootherConfig{Smoother::WeightedJacobi, 2.0 / 3.0}; }
 
+// "jacobi" | "gs" | "sgs" -> the reference's SmootherConfig (multigrid.hpp:55-60)
+SmootherConfig smoother_of(const std::string& name) {
+    if (name == "gs") return SmootherConfig{Smoother::GaussSeidel, 2.0 / 3.0};
+    if (name == "sgs") return SmootherConfig{Smoother::SymmetricGaussSeidel, 2.0 / 3.0};
+    return jacobi();
+}
+
 int cmd_cycles(const Case& c, int k, bool dirichlet, const std::string& rhs, std::uint64_t seed,
                int ncycles, const std::string& smoother) {
     const auto tower = tower_of(c, k);
     MultigridHierarchy h = build_hierarchy(c.base, tower);
-    SmootherConfig sc = jacobi();
-    if (smoother == "gs") sc = SmootherConfig{Smoother::GaussSeidel, 2.0 / 3.0};
-    CyclePlan plan = standard_plan(h.levels(), CycleKind::V, 2, 2, sc);
+    CyclePlan plan = standard_plan(h.levels(), CycleKind::V, 2, 2, smoother_of(smoother));
     plan.cycles = ncycles;
     const auto& m = *h.level(0).mesh;
     MultigridHierarchy::CycleResult out;
@@ -410,10 +415,10 @@ int cmd_cycles(const Case& c, int k, bool dirichlet, const std::string& rhs, std
 }
 
 int cmd_solve(const Case& c, int k, bool dirichlet, const std::string& rhs, std::uint64_t seed,
-              double tol, int maxc) {
+              double tol, int maxc, const std::string& smoother) {
     const auto tower = tower_of(c, k);
     MultigridHierarchy h = build_hierarchy(c.base, tower);
-    CyclePlan plan = standard_plan(h.levels(), CycleKind::V, 2, 2, jacobi());
+    CyclePlan plan = standard_plan(h.levels(), CycleKind::V, 2, 2, smoother_of(smoother));
     const auto& m = *h.level(0).mesh;
     std::vector<double> hist, x;
     int iters = 0;
@@ -461,9 +466,7 @@ int cmd_time(const Case& c, int k, bool dirichlet, int nrhs, int ncyc, double to
     const auto tower = tower_of(c, k);
     MultigridHierarchy h = build_hierarchy(c.base, tower);
     const double setup_s = since(t0);
-    SmootherConfig sc = jacobi();
-    if (smoother == "gs") sc = SmootherConfig{Smoother::GaussSeidel, 2.0 / 3.0};
-    CyclePlan plan = standard_plan(h.levels(), CycleKind::V, 2, 2, sc);
+    CyclePlan plan = standard_plan(h.levels(), CycleKind::V, 2, 2, smoother_of(smoother));
     const auto& m = *h.level(0).mesh;
     const int n = m.num_vertices();
     double t_cycles_small = 0, t_cycles_big = 0, t_solve = 0;
@@ -508,9 +511,9 @@ int main(int argc, char** argv) {
         if (argc < 4) {
             std::fprintf(stderr,
                          "usage: ref_harness structure <case> <k> <bc> [full]\n"
-                         "       ref_harness cycles <case> <k> <bc> <rhs> <seed> <ncycles> [jacobi|gs]\n"
-                         "       ref_harness solve <case> <k> <bc> <rhs> <seed> <tol> <maxc>\n"
-                         "       ref_harness time <case> <k> <bc> <nrhs> <ncyc> <tol> <maxc> [jacobi|gs]\n");
+                         "       ref_harness cycles <case> <k> <bc> <rhs> <seed> <ncycles> [jacobi|gs|sgs]\n"
+                         "       ref_harness solve <case> <k> <bc> <rhs> <seed> <tol> <maxc> [jacobi|gs|sgs]\n"
+                         "       ref_harness time <case> <k> <bc> <nrhs> <ncyc> <tol> <maxc> [jacobi|gs|sgs]\n");
             return 2;
         }
         const std::string cmd = argv[1];
@@ -523,7 +526,7 @@ int main(int argc, char** argv) {
                               std::atoi(argv[7]), argc > 8 ? argv[8] : "jacobi");
         if (cmd == "solve")
             return cmd_solve(c, k, dirichlet, argv[5], std::strtoull(argv[6], nullptr, 10),
-                             std::atof(argv[7]), std::atoi(argv[8]));
+                             std::atof(argv[7]), std::atoi(argv[8]), argc > 9 ? argv[9] : "jacobi");
         if (cmd == "time")
             return cmd_time(c, k, dirichlet, std::atoi(argv[5]), std::atoi(argv[6]),
                             std::atof(argv[7]), std::atoi(argv[8]), argc > 9 ? argv[9] : "jacobi");

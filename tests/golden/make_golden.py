@@ -41,6 +41,10 @@ CYCLES = [
     ("cycles_ico_5_ylm", ["cycles", "ico", "5", "neumann", "ylm", "2", "8"]),
     ("cycles_equi_4_8_3_lr", ["cycles", "equi:4:8:1.0", "3", "neumann", "lr", "3", "10"]),
     ("cycles_ico_3_uniform_gs", ["cycles", "ico", "3", "neumann", "uniform", "4", "6", "gs"]),
+    ("cycles_ico_3_uniform_sgs", ["cycles", "ico", "3", "neumann", "uniform", "4", "6", "sgs"]),
+    ("cycles_ico_5_ylm_gs", ["cycles", "ico", "5", "neumann", "ylm", "2", "5", "gs"]),
+    ("cycles_square_4_dirichlet_sinsin_gs", ["cycles", "square", "4", "dirichlet", "sinsin", "0", "8", "gs"]),
+    ("cycles_equi_4_8_3_lr_sgs", ["cycles", "equi:4:8:1.0", "3", "neumann", "lr", "3", "6", "sgs"]),
 ]
 SOLVES = [
     # BASELINE configs 1-3 (config 3 takes ~30 s of reference setup)
@@ -49,6 +53,8 @@ SOLVES = [
     ("solve_config3", ["solve", "ico", "8", "neumann", "uniform", "1", "1e-8", "200"]),
     ("solve_equi_4_8_3_lr", ["solve", "equi:4:8:1.0", "3", "neumann", "lr", "23", "1e-10", "50"]),
     ("solve_square_6_uniform", ["solve", "square", "6", "neumann", "uniform", "5", "1e-8", "200"]),
+    ("solve_config2_gs", ["solve", "ico", "6", "neumann", "ylm", "1", "1e-8", "200", "gs"]),
+    ("solve_config1_sgs", ["solve", "square", "4", "dirichlet", "sinsin", "0", "1e-8", "200", "sgs"]),
 ]
 
 
@@ -60,7 +66,10 @@ def run(argv):
 def main() -> int:
     if not HARNESS.exists():
         subprocess.run(["make", "-C", str(ROOT / "oracle"), "ref", "-j8"], check=True)
+    only = set(sys.argv[1:])  # optional: regenerate just these stems
     for stem, argv in STRUCTURE + CYCLES + SOLVES:
+        if only and stem not in only:
+            continue
         data = run(argv)
         data["_argv"] = argv
         (OUT / f"{stem}.json").write_text(json.dumps(data, separators=(",", ":")) + "\n")

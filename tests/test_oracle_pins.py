@@ -62,6 +62,7 @@ def test_structure_matches_reference(stem):
 
 
 CYC = sorted(p.stem for p in GOLDEN.glob("cycles_*.json"))
+SMOOTHERS = {"jacobi": 0, "gs": 1, "sgs": 2}  # orc_run_cycles / ref_harness smoother names
 
 
 @pytest.mark.parametrize("stem", CYC)
@@ -70,7 +71,7 @@ def test_cycles_match_reference_bitwise(stem):
     argv = g["_argv"]
     h = hier_from_argv(argv)
     kind, seed, ncyc = argv[4], int(argv[5]), int(argv[6])
-    smoother = 1 if len(argv) > 7 and argv[7] == "gs" else 0
+    smoother = SMOOTHERS[argv[7]] if len(argv) > 7 else 0
     b = h.rhs(kind, seed)
     if not h.dirichlet:
         b = h.project(b)
@@ -89,8 +90,9 @@ def test_gmg_solve_matches_reference_bitwise(stem):
     argv = g["_argv"]
     h = hier_from_argv(argv)
     kind, seed, tol, maxc = argv[4], int(argv[5]), float(argv[6]), int(argv[7])
+    smoother = SMOOTHERS[argv[8]] if len(argv) > 8 else 0
     b = h.rhs(kind, seed)
-    x, hist, iters, final = h.solve(b, tol=tol, max_cycles=maxc)
+    x, hist, iters, final = h.solve(b, tol=tol, max_cycles=maxc, smoother=smoother)
     assert iters == g["iterations"]
     np.testing.assert_array_equal(hist, np.array(g["history"]))
     assert final == g["final"]
