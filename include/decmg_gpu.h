@@ -97,8 +97,13 @@ DECMG_API const char* decmg_gpu_last_error(const decmg_gpu_ctx* ctx);
 
 /* CyclePlan (proj/include/decmg/multigrid.hpp:70-89). walk: 'd'/'u' string
  * (NULL = the V walk of standard_plan, multigrid.cpp:171-194); pre/post:
- * per-level sweep counts (NULL = pre_all/post_all on every level). */
-enum { DECMG_SMOOTHER_JACOBI = 0 };
+ * per-level sweep counts (NULL = pre_all/post_all on every level).
+ * smoother (SmootherConfig, multigrid.hpp:55-60; smooth, multigrid.cpp:95-120):
+ * weighted Jacobi, Gauss-Seidel (forward lexicographic, bit-identical to the
+ * sequential sweep via a level schedule) or symmetric Gauss-Seidel (forward +
+ * reverse per iteration); the reference's fixed-iteration CG smoother is not
+ * offered. The partitioned solve (decmg_gpu_dist_*) runs Jacobi only. */
+enum { DECMG_SMOOTHER_JACOBI = 0, DECMG_SMOOTHER_GS = 1, DECMG_SMOOTHER_SGS = 2 };
 typedef struct {
     const char* walk;
     const int* pre;

@@ -114,6 +114,12 @@ struct Level {
     int* S2_halo = nullptr;  // ELL row indices of halo rows
     int* S2_slot = nullptr;  // [npad * Le_w]
     int S2_maxhalo = -1;     // -1: no tiles
+    // Exact lexicographic Gauss-Seidel as a level schedule (setup.cu
+    // build_gs_schedule): phase p of the forward (f) / reverse (r) sweep is
+    // the internal rows gs?_rows[gs?_ptr[p] .. gs?_ptr[p+1]), ascending.
+    int* gsf_rows = nullptr;
+    int* gsr_rows = nullptr;
+    std::vector<int> gsf_ptr, gsr_ptr;
     int* Re_row = nullptr;   // coarse row q per ELL row of Re (-1 = padding)
     int zero_diag_row = -1;  // first row with L_ii == 0 (-1: none)
     double wtot = 0.0;       // sum of dual areas, sequential (coarse solve)

@@ -883,6 +883,8 @@ int decmg_gpu_dist_run(decmg_gpu_dist* D, const decmg_gpu_plan* plan, int nrhs, 
     cudaSetDevice(D->g->device);
     Plan p;
     Status s = make_plan(D->g.get(), plan, &p);
+    if (s.ok() && p.smoother != DECMG_SMOOTHER_JACOBI)
+        s = Status::Err(DECMG_INVALID_ARGUMENT, "partitioned solve: only the weighted Jacobi smoother");
     if (s.ok()) s = dist_run(D, p, nrhs, b, x0, max_cycles, solve != 0, tol, x_out, hist_out, cycles_done, final_out);
     if (!s.ok()) {
         D->err = s.msg;

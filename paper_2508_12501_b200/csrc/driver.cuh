@@ -141,9 +141,54 @@ struct Driver {
         return Status::Ok();
     }
 
+    // One exact Gauss-Seidel sweep on level k: its phases in order, x in place.
+    Status gs_sweep(int k, bool reverse) {
+        DG_TRY(ensure_x(k));
+        Level& L = c->lv[k];
+        const std::vector<int>& ptr = reverse ? L.gsr_ptr : L.gsf_ptr;
+        const int* rows = reverse ? L.gsr_rows : L.gsf_rows;
+        if (!rows) return Status::Err(DECMG_RUNTIME, "gauss_seidel: no schedule on this level");
+        double* x = xcur(L);
+        const double* b = bptr(k);
+        const bool ell = L.Le_ci && tpr <= 8;
+        const int cls = k == 0 ? kFineSweep : kCoarseLevels;
+        for (size_t p = 0; p + 1 < ptr.size(); ++p) {
+            const int nr = ptr[p + 1] - ptr[p];
+            if (nr == 0) continue;
+            const double bytes = 12.0 * L.nnzL * nr / L.nv + 8.0 * nr + 24.0 * nr * nrhs;
+            const int* rp = rows + ptr[p];
+            DG_TRY(launch(c, cls, bytes, [&] {
+                const unsigned g = grid_for(static_cast<int64_t>(nr) * tpr, kBlock);
+                DISPATCH_BP(key, {
+                    if (ell && L.Le_w == 7)
+                        k_gs_phase<BP, RPT, 7><<<g, kBlock, 0, c->stream>>>(nr, rp, nrhs, nullptr, L.Le_ci, L.Le_v,
+                                                                            L.Le_row, x, b);
+                    else if (ell)
+                        k_gs_phase<BP, RPT, 8><<<g, kBlock, 0, c->stream>>>(nr, rp, nrhs, nullptr, L.Le_ci, L.Le_v,
+                                                                            L.Le_row, x, b);
+                    else
+                        k_gs_phase<BP, RPT, 0><<<g, kBlock, 0, c->stream>>>(nr, rp, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v,
+                                                                            nullptr, x, b);
+                })
+            }));
+        }
+        L.x_zero = false;
+        return Status::Ok();
+    }
+
     Status smooth(int k, int iters, const Plan& plan) {
         Level& L = c->lv[k];
         if (iters <= 0) return Status::Ok();
+        if (plan.smoother != DECMG_SMOOTHER_JACOBI) {  // smooth (multigrid.cpp:95-120)
+            if (L.zero_diag_row >= 0)
+                return Status::Err(DECMG_RUNTIME,
+                                   "gauss_seidel: zero diagonal at row " + std::to_string(L.zero_diag_row));
+            for (int it = 0; it < iters; ++it) {
+                DG_TRY(gs_sweep(k, false));
+                if (plan.smoother == DECMG_SMOOTHER_SGS) DG_TRY(gs_sweep(k, true));
+            }
+            return Status::Ok();
+        }
         if (L.zero_diag_row >= 0)
             return Status::Err(DECMG_RUNTIME, "jacobi: zero diagonal at row " + std::to_string(L.zero_diag_row));
         const double R = nrhs;
@@ -386,7 +431,8 @@ struct Driver {
     // pipelined path and x is materialized)
     bool can_fuse(const Plan& plan) const {
         const Level& L = c->lv[0];
-        return c->lv.size() > 1 && !plan.walk.empty() && plan.walk[0] == 'd' && plan.pre[0] >= 1 && !L.x_zero &&
+        return c->lv.size() > 1 && plan.smoother == DECMG_SMOOTHER_JACOBI && !plan.walk.empty() &&
+               plan.walk[0] == 'd' && plan.pre[0] >= 1 && !L.x_zero &&
                L.Le_ci && tpr <= 8 && L.zero_diag_row < 0;
     }
 

@@ -509,6 +509,32 @@ __global__ void k_perm_fill(int n, const int* __restrict__ ord, const int* __res
     }
 }
 
+// Level schedule of gauss_seidel_sweep (multigrid.cpp:13-34) in the reference
+// numbering: ph[i] = 1 + max ph[j] over neighbours j < i (j > i for the
+// reverse sweep), 0 without such neighbours. Jacobi-style relaxation from 0
+// reaches the fixpoint after depth + 1 steps.
+__global__ void k_gs_phase_step(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                const int* __restrict__ ph_in, int* __restrict__ ph_out, int reverse,
+                                int* changed) {
+    const int64_t i = gtid();
+    if (i >= n) return;
+    int p = 0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        const int j = ci[k];
+        if (reverse ? j > i : j < i) p = max(p, ph_in[j] + 1);
+    }
+    ph_out[i] = p;
+    if (p != ph_in[i]) *changed = 1;
+}
+
+__global__ void k_gs_keys(int n, const int* __restrict__ ord, const int* __restrict__ ph, int* __restrict__ key,
+                          int* __restrict__ q) {
+    const int64_t r = gtid();
+    if (r >= n) return;
+    key[r] = ph[ord ? ord[r] : static_cast<int>(r)];
+    q[r] = static_cast<int>(r);
+}
+
 __global__ void k_invert(int n, const int* __restrict__ ord, int* __restrict__ inv) {
     const int64_t q = gtid();
     if (q < n) inv[ord[q]] = static_cast<int>(q);
@@ -829,6 +855,53 @@ Status build_ell(decmg_gpu_ctx* c, int nrows, const int* rp, const int* ci, cons
     return Status::Ok();
 }
 
+// Phases of the exact Gauss-Seidel sweeps (both directions) and their
+// internal row lists, ascending within a phase (stable radix sort by phase).
+Status build_gs_schedule(decmg_gpu_ctx* c, Level& m) {
+    TmpPool tp(c->stream);
+    const int n = m.nv;
+    int *pa, *pb, *changed, *key, *keys, *qin;
+    DG_TRY(tp.get(&pa, n));
+    DG_TRY(tp.get(&pb, n));
+    DG_TRY(tp.get(&changed, 1));
+    DG_TRY(tp.get(&key, n));
+    DG_TRY(tp.get(&keys, n));
+    DG_TRY(tp.get(&qin, n));
+    for (int reverse = 0; reverse < 2; ++reverse) {
+        DG_CUDA(cudaMemsetAsync(pa, 0, sizeof(int) * n, c->stream));
+        int steps = 0;  // phases never exceed the number of relaxation steps
+        for (;; ++steps) {
+            if (steps > n) return Status::Err(DECMG_RUNTIME, "gauss_seidel: schedule did not converge");
+            DG_CUDA(cudaMemsetAsync(changed, 0, sizeof(int), c->stream));
+            LAUNCH(4, n, k_gs_phase_step, n, m.L_rp, m.L_ci, pa, pb, reverse, changed);
+            std::swap(pa, pb);
+            int h = 0;
+            DG_TRY(read_int(c, changed, &h));
+            if (!h) break;
+        }
+        LAUNCH(4, n, k_gs_keys, n, m.ord, pa, key, qin);
+        int* rows = nullptr;
+        DG_TRY(dalloc(c, &rows, n));
+        int bits = 1;
+        while ((1 << bits) <= steps) ++bits;
+        size_t bytes = 0;
+        DG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key, keys, qin, rows, n, 0, bits, c->stream));
+        char* tmp;
+        DG_TRY(tp.get(&tmp, bytes));
+        DG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, key, keys, qin, rows, n, 0, bits, c->stream));
+        std::vector<int> hk(n);
+        DG_CUDA(cudaMemcpyAsync(hk.data(), keys, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
+        DG_CUDA(cudaStreamSynchronize(c->stream));
+        const int nph = n ? hk[n - 1] + 1 : 0;
+        std::vector<int> ptr(nph + 1, 0);
+        for (int v : hk) ++ptr[v + 1];
+        for (int p = 0; p < nph; ++p) ptr[p + 1] += ptr[p];
+        (reverse ? m.gsr_rows : m.gsf_rows) = rows;
+        (reverse ? m.gsr_ptr : m.gsf_ptr) = std::move(ptr);
+    }
+    return Status::Ok();
+}
+
 // Tiles and halos for the fused sweep pairs (rowkernels.cuh k_sweep2).
 Status build_sweep2(decmg_gpu_ctx* c, Level& m) {
     if (!m.Le_ci || !m.Le_row) return Status::Ok();
@@ -926,6 +999,7 @@ Status build_orders(decmg_gpu_ctx* c) {
         DG_TRY(build_ell(c, cm.nv, m.Ro_rp, m.Ro_ci, m.Ro_v, nullptr, -8, false, &m.Re_ci, &m.Re_v, &m.Re_row,
                          &m.Re_w));
         DG_TRY(build_sweep2(c, m));
+        DG_TRY(build_gs_schedule(c, m));
         if (m.Pe_ci && !m.Le_row) {  // P rows share L's row ids
             m.Pe_ci = nullptr;
             m.Pe_v = nullptr;

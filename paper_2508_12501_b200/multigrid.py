@@ -37,8 +37,11 @@ class Smoother(enum.Enum):
 @dataclass
 class SmootherConfig:
     # The reference default is GaussSeidel (multigrid.hpp:58), a sequential
-    # sweep; the device path implements weighted Jacobi (multigrid.cpp:36-56),
-    # identical in the oracle and on the GPU.
+    # sweep. The device implements weighted Jacobi (multigrid.cpp:36-56) and
+    # the forward / symmetric Gauss-Seidel sweeps (multigrid.cpp:13-34) as a
+    # level schedule that is bit-identical to the sequential sweep (DESIGN.md
+    # "Gauss-Seidel"); the default stays Jacobi (BASELINE north star). Cg is
+    # not offered on the device.
     method: Smoother = Smoother.WeightedJacobi
     jacobi_omega: float = 2.0 / 3.0
 
@@ -168,15 +171,19 @@ def _ptr(a: np.ndarray):
     return a.ctypes.data_as(C.c_void_p)
 
 
+_SMOOTHER_C = {Smoother.WeightedJacobi: 0, Smoother.GaussSeidel: 1, Smoother.SymmetricGaussSeidel: 2}
+
+
 def _plan_struct(plan: CyclePlan, levels: int):
-    if plan.smoother.method != Smoother.WeightedJacobi:
-        raise ValueError("smoother: the device implements weighted Jacobi only")
+    if plan.smoother.method not in _SMOOTHER_C:
+        raise ValueError("smoother: the device implements weighted Jacobi and (symmetric) Gauss-Seidel")
     plan.validate(levels)
     pre = (C.c_int * levels)(*plan.pre[:levels])
     post = (C.c_int * levels)(*plan.post[:levels])
     walk = plan.walk_string().encode()
     s = decmg_gpu_plan(walk=walk, pre=C.cast(pre, C.POINTER(C.c_int)), post=C.cast(post, C.POINTER(C.c_int)),
-                       pre_all=0, post_all=0, smoother=0, jacobi_omega=float(plan.smoother.jacobi_omega))
+                       pre_all=0, post_all=0, smoother=_SMOOTHER_C[plan.smoother.method],
+                       jacobi_omega=float(plan.smoother.jacobi_omega))
     return s, (pre, post, walk)  # keep buffers alive
 
 

@@ -89,10 +89,21 @@ def test_spmv_bitwise_equal_to_reference_apply():
             np.testing.assert_array_equal(h.apply(k, "R", x), o.spmv(k, "R", x))
 
 
-@pytest.mark.parametrize("stem", sorted(p.stem for p in GOLDEN.glob("cycles_*.json") if not p.stem.endswith("_gs")))
+SMOOTHERS = {"jacobi": d.Smoother.WeightedJacobi, "gs": d.Smoother.GaussSeidel,
+             "sgs": d.Smoother.SymmetricGaussSeidel}
+ORC_SMOOTHER = {d.Smoother.WeightedJacobi: 0, d.Smoother.GaussSeidel: 1, d.Smoother.SymmetricGaussSeidel: 2}
+
+
+def smoother_cfg(name):
+    return d.SmootherConfig(method=SMOOTHERS[name])
+
+
+@pytest.mark.parametrize("stem", sorted(p.stem for p in GOLDEN.glob("cycles_*.json")))
 def test_run_cycle_iterates_bitwise_vs_reference(stem):
     """run_cycle (multigrid.cpp:287-323) from the reference's own projected RHS:
-    bit-identical iterate, residual history within 1e-10 relative."""
+    bit-identical iterate, residual history within 1e-10 relative -- weighted
+    Jacobi, and (suffix _gs / _sgs) the reference's sequential Gauss-Seidel
+    sweeps reproduced by the level-scheduled device sweep."""
     g = load(stem)
     argv = g["_argv"]
     h = gpu_from_argv(argv)
@@ -101,7 +112,7 @@ def test_run_cycle_iterates_bitwise_vs_reference(stem):
     if argv[3] != "dirichlet":
         b = o.project(b)
     assert str(fnv(b)) == g["fnv_b"]
-    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother_cfg(argv[7] if len(argv) > 7 else "jacobi"))
     plan.cycles = int(argv[6])
     res = h.run_cycle(plan, b, np.zeros_like(b))
     ref = np.array(g["history"])
@@ -110,10 +121,11 @@ def test_run_cycle_iterates_bitwise_vs_reference(stem):
 
 
 @pytest.mark.parametrize("stem", ["solve_config1", "solve_config2", "solve_config3", "solve_equi_4_8_3_lr",
-                                  "solve_square_6_uniform"])
+                                  "solve_square_6_uniform", "solve_config2_gs", "solve_config1_sgs"])
 def test_gmg_solve_vs_reference(stem):
     """gmg_solve (solvers.cpp:251-279): same cycle count to tol, per-cycle
-    residuals within 1e-10 relative (BASELINE configs 1-3)."""
+    residuals within 1e-10 relative (BASELINE configs 1-3; and with the
+    reference's Gauss-Seidel / symmetric Gauss-Seidel smoothers)."""
     g = load(stem)
     argv = g["_argv"]
     h = gpu_from_argv(argv)
@@ -121,7 +133,7 @@ def test_gmg_solve_vs_reference(stem):
     b = h.make_rhs(kind, seed)
     o = OracleHierarchy(argv[1], int(argv[2]), argv[3] == "dirichlet")
     np.testing.assert_array_equal(b, o.rhs(kind, seed))
-    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother_cfg(argv[8] if len(argv) > 8 else "jacobi"))
     rep = d.gmg_solve(h, plan, b, tol, maxc)
     ref = np.array(g["history"])
     assert abs(rep.iterations - g["iterations"]) <= 1
@@ -399,3 +411,47 @@ def test_kernel_variants_bitwise(monkeypatch, env, base, nsub, dirichlet, nrhs):
     for j in range(nrhs):
         ox, oh = o.run_cycles(B[:, j], ncycles=3)
         np.testing.assert_array_equal(x[:, j], ox)
+
+
+@pytest.mark.parametrize("smoother", ["gs", "sgs"])
+@pytest.mark.parametrize("base,nsub,dirichlet,nrhs", [("ico", 7, False, 16), ("square", 7, True, 1),
+                                                      ("equi:4:8:1.0", 4, False, 3)])
+def test_gauss_seidel_bitwise_vs_oracle(smoother, base, nsub, dirichlet, nrhs):
+    """Level-scheduled Gauss-Seidel (forward and symmetric) against the
+    oracle's sequential sweep at 164 k vertices, batched and Dirichlet; the
+    schedule has a handful of phases per level (setup.cu build_gs_schedule)."""
+    h = d.MultigridHierarchy.from_base(base, nsub, dirichlet=dirichlet, max_nrhs=nrhs)
+    o = OracleHierarchy(base, nsub, dirichlet)
+    if nrhs == 1:
+        B = o.rhs("sinsin" if dirichlet else "uniform", 3)[:, None]
+    else:
+        B = h.make_rhs("uniform", 70, nrhs)
+    if not dirichlet:
+        B = np.stack([o.project(B[:, j]) for j in range(nrhs)], axis=1)
+    cfg = smoother_cfg(smoother)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 1, 1, cfg)
+    plan.cycles = 3
+    res = h.run_cycle(plan, B if nrhs > 1 else B[:, 0])
+    x = res.x if nrhs > 1 else res.x[:, None]
+    hist = res.residual_history if nrhs > 1 else res.residual_history[:, None]
+    for j in range(nrhs):
+        ox, oh = o.run_cycles(B[:, j], ncycles=3, pre=1, post=1, smoother=ORC_SMOOTHER[cfg.method])
+        np.testing.assert_array_equal(x[:, j], ox)
+        assert np.all(np.abs(hist[:, j] - oh) <= RTOL_HIST * oh)
+    # W walk with Gauss-Seidel on every level
+    plan = d.standard_plan(h.levels(), d.CycleKind.W, 2, 1, cfg)
+    plan.cycles = 2
+    res = h.run_cycle(plan, B[:, 0] if nrhs == 1 else B)
+    x = res.x if nrhs > 1 else res.x[:, None]
+    ox, _ = o.run_cycles(B[:, 0], ncycles=2, pre=2, post=1, smoother=ORC_SMOOTHER[cfg.method],
+                         walk=plan.walk_string())
+    np.testing.assert_array_equal(x[:, 0], ox)
+
+
+def test_partitioned_solve_rejects_gauss_seidel():
+    dh = d.DistributedHierarchy("ico", 4, 2)
+    plan = d.standard_plan(dh.levels(), d.CycleKind.V, 2, 2, smoother_cfg("gs"))
+    plan.cycles = 1
+    b = np.zeros(dh.context().n())
+    with pytest.raises(ValueError, match="only the weighted Jacobi"):
+        dh.run_cycle(plan, b)
