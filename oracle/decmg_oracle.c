@@ -825,6 +825,80 @@ int orc_solve(const orc_hier* h, int pre, int post, int smoother, double omega, 
     return rc;
 }
 
+/* gmg_preconditioned_cg (proj/src/solvers.cpp:118-130) = weighted_cg
+ * (solvers.cpp:56-116) on the fine operator with the level-0 dual areas as
+ * weights and run_cycle(inner plan: walk, pre/post, smoother, ncycles cycles,
+ * r, 0) as the preconditioner, after
+ * project_compatible(b). hist_out[0..iters] (iters + 1 entries). Returns -2
+ * with the reference's message on a CG breakdown. */
+static double wdot(const double* w, const double* a, const double* c, int n) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += w[i] * a[i] * c[i];
+    return s;
+}
+
+int orc_pcg(const orc_hier* h, const char* walk, int pre, int post, int smoother, double omega, int ncycles,
+            const double* b, double tol, int maxiter, double* x_out, double* hist_out, int* iters_out,
+            double* final_out) {
+    const level_t* l0 = &h->lv[0];
+    const int n = l0->m.nv;
+    const double* w = l0->area;
+    double* bc = NEW(double, n);
+    memcpy(bc, b, (size_t)n * sizeof(double));
+    orc_project(h, bc);
+    double* x = NEW(double, n);
+    double* r = NEW(double, n);
+    double* z = NEW(double, n);
+    double* p = NEW(double, n);
+    double* Ap = NEW(double, n);
+    double* zero = NEW(double, n);
+    double* hc = NEW(double, ncycles > 0 ? ncycles : 1);
+    int rc = 0, it = 0;
+    csr_apply(n, l0->L_rp, l0->L_ci, l0->L_v, x, r);
+    for (int i = 0; i < n; ++i) r[i] = bc[i] - r[i];
+    const double bn = orc_norm2(bc, n);
+    const double denom = bn > 0.0 ? bn : 1.0;
+    rc = orc_run_cycles(h, walk, pre, post, smoother, omega, r, zero, ncycles, z, hc);
+    memcpy(p, z, (size_t)n * sizeof(double));
+    double rz = wdot(w, r, z, n);
+    double res = orc_norm2(r, n) / denom;
+    if (hist_out) hist_out[0] = res;
+    while (!rc && res > tol && it < maxiter) {
+        csr_apply(n, l0->L_rp, l0->L_ci, l0->L_v, p, Ap);
+        const double curv = wdot(w, p, Ap, n);
+        if (curv == 0.0 || !isfinite(curv)) {
+            set_err("cg: breakdown (zero curvature) at iteration %d", it);
+            rc = -2;
+            break;
+        }
+        const double alpha = rz / curv;
+        if (!isfinite(alpha)) {
+            set_err("cg: breakdown (non-finite step) at iteration %d", it);
+            rc = -2;
+            break;
+        }
+        for (int i = 0; i < n; ++i) x[i] += alpha * p[i];
+        for (int i = 0; i < n; ++i) r[i] -= alpha * Ap[i];
+        rc = orc_run_cycles(h, walk, pre, post, smoother, omega, r, zero, ncycles, z, hc);
+        if (rc) break;
+        const double rz_new = wdot(w, r, z, n);
+        const double beta = rz_new / rz;
+        for (int i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+        rz = rz_new;
+        ++it;
+        res = orc_norm2(r, n) / denom;
+        if (hist_out) hist_out[it] = res;
+    }
+    /* final_relative_residual = relative_residual(A, x, bc) (solvers.cpp:20-27) */
+    csr_apply(n, l0->L_rp, l0->L_ci, l0->L_v, x, Ap);
+    for (int i = 0; i < n; ++i) Ap[i] = bc[i] - Ap[i];
+    if (final_out) *final_out = orc_norm2(Ap, n) / denom;
+    if (iters_out) *iters_out = it;
+    if (x_out) memcpy(x_out, x, (size_t)n * sizeof(double));
+    free(bc); free(x); free(r); free(z); free(p); free(Ap); free(zero); free(hc);
+    return rc;
+}
+
 /* ------------------------------------------------------- RHS (x3) -------- */
 /* std::mt19937_64 (the standard MT19937-64 recurrence) + uniform01 =
  * (rng() >> 11) * 2^-53 (proj/include/decmg/rng.hpp:11-13). */

@@ -457,6 +457,27 @@ int cmd_solve(const Case& c, int k, bool dirichlet, const std::string& rhs, std:
 }
 
 // CPU baseline: the reference protocol (proj/tools/decmg_main.cpp:133-147):
+// gmg_preconditioned_cg (proj/src/solvers.cpp:118-130) with an inner plan
+// standard_plan(levels, V|W, pre, post, smoother), inner.cycles = icyc
+// (Neumann; the reference projects b itself).
+int cmd_pcg(const Case& c, int k, const std::string& rhs, std::uint64_t seed, const std::string& kind, int pre,
+            int post, int icyc, double tol, int maxit, const std::string& smoother) {
+    const auto tower = tower_of(c, k);
+    MultigridHierarchy h = build_hierarchy(c.base, tower);
+    CyclePlan inner = standard_plan(h.levels(), kind == "W" ? CycleKind::W : CycleKind::V, pre, post,
+                                    smoother_of(smoother));
+    inner.cycles = icyc;
+    const auto& m = *h.level(0).mesh;
+    const std::vector<double> b = make_rhs(rhs, m, h.fine_operator(), seed, nullptr);
+    const SolveReport rep = gmg_preconditioned_cg(h, inner, b, tol, maxit);
+    std::printf("{\"n\": %d, \"iterations\": %d, \"converged\": %s, \"final\": %.17g, \"fnv_x\": \"%llu\",\n",
+                (int)b.size(), rep.iterations, rep.converged ? "true" : "false", rep.final_relative_residual,
+                (unsigned long long)fnv_vec(rep.solution));
+    print_dvec("history", rep.residual_history, false);
+    std::printf("}\n");
+    return 0;
+}
+
 // per-cycle cost = (t(2n) - t(n)) / n with run_cycle from x0 = 0, plus a full
 // gmg_solve. nrhs independent right-hand sides are solved one after another
 // (the reference has no batched solve).
@@ -513,7 +534,8 @@ int main(int argc, char** argv) {
                          "usage: ref_harness structure <case> <k> <bc> [full]\n"
                          "       ref_harness cycles <case> <k> <bc> <rhs> <seed> <ncycles> [jacobi|gs|sgs]\n"
                          "       ref_harness solve <case> <k> <bc> <rhs> <seed> <tol> <maxc> [jacobi|gs|sgs]\n"
-                         "       ref_harness time <case> <k> <bc> <nrhs> <ncyc> <tol> <maxc> [jacobi|gs|sgs]\n");
+                         "       ref_harness time <case> <k> <bc> <nrhs> <ncyc> <tol> <maxc> [jacobi|gs|sgs]\n"
+                         "       ref_harness pcg <case> <k> neumann <rhs> <seed> <V|W> <pre> <post> <cycles> <tol> <maxit> [jacobi|gs|sgs]\n");
             return 2;
         }
         const std::string cmd = argv[1];
@@ -521,6 +543,10 @@ int main(int argc, char** argv) {
         const int k = std::atoi(argv[3]);
         const bool dirichlet = argc > 4 && std::string(argv[4]) == "dirichlet";
         if (cmd == "structure") return cmd_structure(c, k, dirichlet, argc > 5 && std::string(argv[5]) == "full");
+        if (cmd == "pcg" && argc >= 13)
+            return cmd_pcg(c, k, argv[5], std::strtoull(argv[6], nullptr, 10), argv[7], std::atoi(argv[8]),
+                           std::atoi(argv[9]), std::atoi(argv[10]), std::atof(argv[11]), std::atoi(argv[12]),
+                           argc > 13 ? argv[13] : "jacobi");
         if (cmd == "cycles")
             return cmd_cycles(c, k, dirichlet, argv[5], std::strtoull(argv[6], nullptr, 10),
                               std::atoi(argv[7]), argc > 8 ? argv[8] : "jacobi");

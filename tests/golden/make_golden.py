@@ -56,6 +56,14 @@ SOLVES = [
     ("solve_config2_gs", ["solve", "ico", "6", "neumann", "ylm", "1", "1e-8", "200", "gs"]),
     ("solve_config1_sgs", ["solve", "square", "4", "dirichlet", "sinsin", "0", "1e-8", "200", "sgs"]),
 ]
+PCG = [
+    # gmg_preconditioned_cg (solvers.cpp:118-130): <rhs> <seed> <V|W> <pre> <post> <cycles> <tol> <maxit> [smoother]
+    ("pcg_config2_v22", ["pcg", "ico", "6", "neumann", "ylm", "1", "V", "2", "2", "1", "1e-8", "100"]),
+    ("pcg_ico_5_w22x2", ["pcg", "ico", "5", "neumann", "uniform", "13", "W", "2", "2", "2", "1e-9", "100"]),
+    ("pcg_square_5_uniform_v11_sgs", ["pcg", "square", "5", "neumann", "uniform", "8", "V", "1", "1", "1", "1e-9",
+                                      "100", "sgs"]),
+    ("pcg_equi_onelevel", ["pcg", "equi:4:8:1.0", "0", "neumann", "uniform", "7", "V", "3", "3", "1", "1e-9", "30"]),
+]
 
 
 def run(argv):
@@ -67,7 +75,7 @@ def main() -> int:
     if not HARNESS.exists():
         subprocess.run(["make", "-C", str(ROOT / "oracle"), "ref", "-j8"], check=True)
     only = set(sys.argv[1:])  # optional: regenerate just these stems
-    for stem, argv in STRUCTURE + CYCLES + SOLVES:
+    for stem, argv in STRUCTURE + CYCLES + SOLVES + PCG:
         if only and stem not in only:
             continue
         data = run(argv)

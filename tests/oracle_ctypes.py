@@ -53,6 +53,8 @@ def lib() -> C.CDLL:
                                 C.c_double, C.c_int, C.c_void_p, C.c_void_p,
                                 C.POINTER(C.c_int), C.POINTER(C.c_double)]
         L.orc_coarse_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_pcg.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                              C.c_void_p, C.c_double, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 
@@ -146,6 +148,20 @@ class OracleHierarchy:
         if rc:
             raise RuntimeError(lib().orc_last_error().decode())
         return x, hist[: it.value], it.value, fin.value
+
+    def pcg(self, b, tol, maxiter, walk=None, pre=2, post=2, smoother=0, omega=2.0 / 3.0, cycles=1):
+        """gmg_preconditioned_cg (solvers.cpp:118-130): (x, history[iters+1], iters, final)."""
+        n = self.n()
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty(n)
+        hist = np.empty(maxiter + 1)
+        it = C.c_int()
+        fin = C.c_double()
+        rc = lib().orc_pcg(self.h, None if walk is None else walk.encode(), pre, post, smoother, omega, cycles,
+                           _p(b), tol, maxiter, _p(x), _p(hist), C.byref(it), C.byref(fin))
+        if rc:
+            raise RuntimeError(lib().orc_last_error().decode())
+        return x, hist[: it.value + 1], it.value, fin.value
 
     def coarse_solve(self, b):
         b = np.ascontiguousarray(b, dtype=np.float64)

@@ -97,3 +97,31 @@ def test_gmg_solve_matches_reference_bitwise(stem):
     np.testing.assert_array_equal(hist, np.array(g["history"]))
     assert final == g["final"]
     assert str(fnv(x)) == g["fnv_x"]
+
+
+PCG = sorted(p.stem for p in GOLDEN.glob("pcg_*.json"))
+
+
+def w_walk(levels):
+    """standard_plan's W walk (multigrid.cpp:149-194, emit_solve with gamma 2)."""
+    import paper_2508_12501_b200 as d
+    return d.standard_plan(levels, d.CycleKind.W, 1, 1).walk_string()
+
+
+@pytest.mark.parametrize("stem", PCG)
+def test_pcg_matches_reference_bitwise(stem):
+    """gmg_preconditioned_cg: the oracle reproduces the reference's iterations,
+    history, final residual and solution bit for bit."""
+    g = load(stem)
+    argv = g["_argv"]
+    h = hier_from_argv(argv)
+    kind, seed, ck, pre, post, cyc, tol, maxit = (argv[4], int(argv[5]), argv[6], int(argv[7]), int(argv[8]),
+                                                  int(argv[9]), float(argv[10]), int(argv[11]))
+    smoother = SMOOTHERS[argv[12]] if len(argv) > 12 else 0
+    b = h.rhs(kind, seed)
+    walk = w_walk(h.levels) if ck == "W" else None
+    x, hist, iters, final = h.pcg(b, tol, maxit, walk=walk, pre=pre, post=post, smoother=smoother, cycles=cyc)
+    assert iters == g["iterations"]
+    np.testing.assert_array_equal(hist, np.array(g["history"]))
+    assert final == g["final"]
+    assert str(fnv(x)) == g["fnv_x"]
