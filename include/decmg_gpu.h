@@ -128,6 +128,19 @@ DECMG_API int decmg_gpu_solve(decmg_gpu_ctx* ctx, const decmg_gpu_plan* plan, in
                     const double* x0, double tol, int max_cycles, double* x_out, double* hist_out,
                     int* cycles_done, double* final_out);
 
+/* gmg_preconditioned_cg (proj/src/solvers.cpp:118-130): weighted CG
+ * (solvers.cpp:56-116, dual-area weights) preconditioned by inner_cycles
+ * cycles of the inner plan from zero; projects b (Neumann hierarchies only).
+ * hist_out [maxiter+1][nrhs] (entry 0 = initial residual; rows past
+ * iters_out[l] of lane l untouched); iters_out, converged_out, final_out
+ * [nrhs] (final = recomputed relative residual of the solution). Weighted
+ * dots are deterministic trees, not the reference's sequential sums: iterates
+ * agree to rounding, histories within 1e-10. A CG
+ * breakdown returns DECMG_RUNTIME with the reference's message. */
+DECMG_API int decmg_gpu_pcg(decmg_gpu_ctx* ctx, const decmg_gpu_plan* inner, int inner_cycles, int nrhs,
+                            const double* b, double tol, int maxiter, double* x_out, double* hist_out,
+                            int* iters_out, int* converged_out, double* final_out);
+
 /* Device-pointer variants (inputs already resident in HBM). hist/final are
  * device arrays too. */
 DECMG_API int decmg_gpu_run_cycles_dev(decmg_gpu_ctx* ctx, const decmg_gpu_plan* plan, int nrhs,

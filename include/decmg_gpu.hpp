@@ -222,4 +222,29 @@ inline SolveReport gmg_solve(const MultigridHierarchy& h, const CyclePlan& plan,
     return rep;
 }
 
+// gmg_preconditioned_cg (proj/src/solvers.cpp:118-130); inner_plan.cycles
+// cycles of the inner plan precondition each CG step. Single RHS, like the
+// reference; the C ABI (decmg_gpu_pcg) also takes [n][nrhs] batches.
+inline SolveReport gmg_preconditioned_cg(const MultigridHierarchy& h, const CyclePlan& inner_plan,
+                                         const std::vector<double>& b, double tol, int maxiter) {
+    const auto t0 = std::chrono::steady_clock::now();
+    inner_plan.validate(h.levels());
+    if (static_cast<int>(b.size()) != h.fine_rows()) throw std::invalid_argument("run_cycle: rhs size mismatch");
+    detail::PlanC pc(inner_plan);
+    SolveReport rep;
+    rep.solution.resize(b.size());
+    std::vector<double> hist(static_cast<size_t>(maxiter > 0 ? maxiter : 0) + 1);
+    int its = 0, conv = 0;
+    double fin = 0.0;
+    detail::check(decmg_gpu_pcg(h.handle(), &pc.s, inner_plan.cycles, 1, b.data(), tol, maxiter,
+                                rep.solution.data(), hist.data(), &its, &conv, &fin),
+                  h.handle());
+    rep.residual_history.assign(hist.begin(), hist.begin() + its + 1);
+    rep.iterations = its;
+    rep.converged = conv != 0;
+    rep.final_relative_residual = fin;
+    rep.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return rep;
+}
+
 }  // namespace decmg

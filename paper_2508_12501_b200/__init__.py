@@ -7,9 +7,10 @@ reference's C++ multigrid API; it has no CPU implementation of the path.
 """
 from ._lib import DecmgError, CudaError, LIB_PATH, load as load_library
 from .multigrid import (CycleKind, CyclePlan, CycleResult, DistributedHierarchy, MultigridHierarchy, Smoother,
-                        SmootherConfig, SolveReport, Transition, base_mesh, build_hierarchy, gmg_solve,
-                        nccl_unique_id, standard_plan)
+                        SmootherConfig, SolveReport, Transition, base_mesh, build_hierarchy, gmg_preconditioned_cg,
+                        gmg_solve, nccl_unique_id, standard_plan)
 
 __all__ = ["CycleKind", "CyclePlan", "CycleResult", "DistributedHierarchy", "MultigridHierarchy", "nccl_unique_id", "Smoother", "SmootherConfig",
-           "SolveReport", "Transition", "base_mesh", "build_hierarchy", "gmg_solve", "standard_plan",
+           "SolveReport", "Transition", "base_mesh", "build_hierarchy", "gmg_preconditioned_cg", "gmg_solve",
+           "standard_plan",
            "DecmgError", "CudaError", "LIB_PATH", "load_library"]

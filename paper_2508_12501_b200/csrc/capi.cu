@@ -225,6 +225,27 @@ int decmg_gpu_solve(decmg_gpu_ctx* ctx, const decmg_gpu_plan* plan, int nrhs, co
     return DECMG_OK;
 }
 
+int decmg_gpu_pcg(decmg_gpu_ctx* ctx, const decmg_gpu_plan* inner, int inner_cycles, int nrhs, const double* b,
+                  double tol, int maxiter, double* x_out, double* hist_out, int* iters_out, int* converged_out,
+                  double* final_out) {
+    if (!ctx) return DECMG_INVALID_ARGUMENT;
+    if (!b || !iters_out || !converged_out)
+        return fail(ctx, Status::Err(DECMG_INVALID_ARGUMENT, "gmg_pcg: null argument"));
+    cudaSetDevice(ctx->device);
+    Plan p;
+    API_TRY(ctx, make_plan(ctx, inner, &p));
+    if (nrhs < 1 || nrhs > ctx->max_nrhs)
+        return fail(ctx, Status::Err(DECMG_INVALID_ARGUMENT, "nrhs must be in [1, max_nrhs]"));
+    const size_t n = static_cast<size_t>(ctx->lv[0].nv) * nrhs;
+    API_TRY(ctx, cuda_status(cudaMemcpyAsync(ctx->io_b, b, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D b"));
+    API_TRY(ctx, pcg(ctx, p, inner_cycles, nrhs, ctx->io_b, tol, maxiter, ctx->io_x, hist_out, iters_out,
+                     converged_out, final_out));
+    if (x_out)
+        API_TRY(ctx, cuda_status(cudaMemcpyAsync(x_out, ctx->io_x, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H x"));
+    API_TRY(ctx, cuda_status(cudaStreamSynchronize(ctx->stream), "gmg_pcg"));
+    return DECMG_OK;
+}
+
 int decmg_gpu_project_compatible(decmg_gpu_ctx* ctx, int nrhs, double* b) {
     if (!ctx || !b) return DECMG_INVALID_ARGUMENT;
     cudaSetDevice(ctx->device);

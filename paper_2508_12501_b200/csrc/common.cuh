@@ -85,6 +85,7 @@ struct Level {
     int* ord = nullptr;      // [nv] internal row -> vertex
     int* inv = nullptr;      // [nv] vertex -> internal row
     double* diag_i = nullptr;  // L_ii by internal row (== diag without ord)
+    double* area_i = nullptr;  // dual areas by internal row (== area without ord)
     int* bd_i = nullptr;       // boundary flag by internal row (== bd without ord)
     int* Lo_rp = nullptr;
     int* Lo_ci = nullptr;
@@ -166,6 +167,8 @@ struct decmg_gpu_ctx {
     double* io_b = nullptr;     // staging for host-pointer calls [n0][max_nrhs]
     double* io_x0 = nullptr;
     double* io_x = nullptr;
+    double* pcg_buf = nullptr;  // GMG-PCG vectors (pcg.cu), 5 x [n0][max_nrhs], allocated on first use
+    double* pcg_s = nullptr;    // GMG-PCG per-lane scalars [8][32]
     cudaStream_t io_stream = nullptr;        // chunked host copies (stage_rhs)
     std::vector<cudaEvent_t> io_events;
     int64_t launch_count = 0;
@@ -238,6 +241,9 @@ Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, co
              double tol, int max_cycles, double* d_x, double* h_hist, int* cycles_done,
              double* h_final, bool staged = false);
 Status stage_rhs(decmg_gpu_ctx* c, int nrhs, const double* h_b, bool project);
+// pcg.cu: gmg_preconditioned_cg (proj/src/solvers.cpp:118-130)
+Status pcg(decmg_gpu_ctx* c, const Plan& inner, int inner_cycles, int nrhs, const double* d_b, double tol,
+           int maxiter, double* d_x, double* h_hist, int* iters, int* converged, double* h_final);
 Status project_compatible(decmg_gpu_ctx* c, int nrhs, double* d_b);
 Status apply_op(decmg_gpu_ctx* c, int level, char op, const double* d_x, double* d_y);
 

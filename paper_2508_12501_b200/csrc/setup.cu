@@ -977,12 +977,15 @@ Status build_orders(decmg_gpu_ctx* c) {
         if (m.ord) {
             DG_TRY(dalloc(c, &m.diag_i, m.nv));
             LAUNCH(4, m.nv, k_take<double>, m.nv, m.ord, m.diag, m.diag_i);
+            DG_TRY(dalloc(c, &m.area_i, m.nv));
+            LAUNCH(4, m.nv, k_take<double>, m.nv, m.ord, m.area, m.area_i);
             if (m.bd) {
                 DG_TRY(dalloc(c, &m.bd_i, m.nv));
                 LAUNCH(4, m.nv, k_take<int>, m.nv, m.ord, m.bd, m.bd_i);
             }
         } else {
             m.diag_i = m.diag;
+            m.area_i = m.area;
             m.bd_i = m.bd;
         }
         if (k + 1 < L) {

@@ -422,6 +422,36 @@ def gmg_solve(h: MultigridHierarchy, plan: CyclePlan, b: np.ndarray, tol: float,
                        final_relative_residual=final.tolist(), wall_seconds=wall)
 
 
+def gmg_preconditioned_cg(h: MultigridHierarchy, inner_plan: CyclePlan, b: np.ndarray, tol: float,
+                          maxiter: int) -> SolveReport:
+    """gmg_preconditioned_cg (solvers.cpp:118-130): weighted CG on the fine
+    operator (dual-area inner product) preconditioned by inner_plan.cycles
+    cycles of inner_plan from zero; b is projected first (Neumann only).
+    residual_history has iterations + 1 entries (the initial residual first);
+    final_relative_residual is recomputed from the solution. A CG breakdown
+    raises RuntimeError with the reference's message."""
+    t0 = time.perf_counter()
+    n = h.n()
+    b, nrhs = h._vec(b, n)
+    ps, keep = _plan_struct(inner_plan, h.levels())
+    x = np.empty_like(b)
+    hist = np.zeros((maxiter + 1, nrhs))
+    its = np.zeros(nrhs, dtype=np.int32)
+    conv = np.zeros(nrhs, dtype=np.int32)
+    final = np.zeros(nrhs)
+    check(h._lib.decmg_gpu_pcg(h.ctx, C.byref(ps), int(inner_plan.cycles), nrhs, _ptr(b), tol, maxiter, _ptr(x),
+                               _ptr(hist), _ptr(its), _ptr(conv), _ptr(final)), h.ctx)
+    wall = time.perf_counter() - t0
+    if b.ndim == 1:
+        it = int(its[0])
+        return SolveReport(solution=x, residual_history=hist[: it + 1, 0].tolist(), cumulative_seconds=[],
+                           iterations=it, converged=bool(conv[0]), final_relative_residual=float(final[0]),
+                           wall_seconds=wall)
+    return SolveReport(solution=x, residual_history=[hist[: its[j] + 1, j].tolist() for j in range(nrhs)],
+                       cumulative_seconds=[], iterations=its.tolist(), converged=[bool(v) for v in conv],
+                       final_relative_residual=final.tolist(), wall_seconds=wall)
+
+
 class DistributedHierarchy:
     """Vertex-partitioned multi-GPU hierarchy.
 
