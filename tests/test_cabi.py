@@ -45,7 +45,19 @@ def test_library_is_sm100a():
 
 def test_cpp_shim_compiles():
     shim = ROOT / "include" / "decmg_gpu.hpp"
-    src = '#include "decmg_gpu.hpp"\nint main(){ auto p = decmg::standard_plan(3, decmg::CycleKind::W); return p.walk.size() == 6 ? 0 : 1; }\n'
+    src = """#include "decmg_gpu.hpp"
+int main() {
+    auto p = decmg::standard_plan(3, decmg::CycleKind::W);
+    auto gs = decmg::standard_plan(3, decmg::CycleKind::V, 2, 2,
+                                   decmg::SmootherConfig{decmg::Smoother::GaussSeidel});
+    // the GPU entry points must at least compile and link (no device here)
+    auto solve = &decmg::gmg_solve;
+    auto pcg = &decmg::gmg_preconditioned_cg;
+    (void)solve;
+    (void)pcg;
+    return p.walk.size() == 6 && gs.smoother.method == decmg::Smoother::GaussSeidel ? 0 : 1;
+}
+"""
     exe = ROOT / "build" / "shim_test"
     exe.parent.mkdir(exist_ok=True)
     (exe.parent / "shim_test.cpp").write_text(src)
