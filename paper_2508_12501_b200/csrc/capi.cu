@@ -39,6 +39,7 @@ Status init_ctx(decmg_gpu_ctx* c, const decmg_gpu_config* cfg) {
     if (const char* e = std::getenv("DECMG_SWEEP2")) c->sweep2 = std::atoi(e) != 0;
     if (const char* e = std::getenv("DECMG_PF")) c->pf = std::atoi(e);
     if (const char* e = std::getenv("DECMG_FUSE_RR")) c->fuse_rr = std::atoi(e) != 0;
+    if (const char* e = std::getenv("DECMG_RR_WINDOW")) c->rr_window = std::atoi(e) != 0;
     if (const char* e = std::getenv("DECMG_PFL")) c->pfl = std::atoi(e);
     if (const char* e = std::getenv("DECMG_KERNEL")) {
         const std::string m(e);

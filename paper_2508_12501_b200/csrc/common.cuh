@@ -118,6 +118,12 @@ struct Level {
     // Exact lexicographic Gauss-Seidel as a level schedule (setup.cu
     // build_gs_schedule): phase p of the forward (f) / reverse (r) sweep is
     // the internal rows gs?_rows[gs?_ptr[p] .. gs?_ptr[p+1]), ascending.
+    // Fused residual + restriction (rowkernels.cuh k_res_restrict): coarse
+    // rows sorted by the fine internal row of their first R column, and per
+    // granule of 4 fine rows the first index into rr_crows (rr_ngran + 1).
+    int* rr_crows = nullptr;
+    int* rr_gptr = nullptr;
+    int rr_ngran = 0;
     int* gsf_rows = nullptr;
     int* gsr_rows = nullptr;
     std::vector<int> gsf_ptr, gsr_ptr;
@@ -179,6 +185,7 @@ struct decmg_gpu_ctx {
     int pf = 56;                // row-kernel prefetch distance in rows, 0 = off (env DECMG_PF)
     int pfl = 2;                // prefetch into L1 (1) or L2 (2) (env DECMG_PFL)
     int fuse_rr = 0;            // residual recomputed inside the restriction, opt-in (env DECMG_FUSE_RR=1; slower)
+    int rr_window = 0;          // residual + restriction through a shared-memory window, opt-in (env DECMG_RR_WINDOW=1; slower)
     int kmode = 2;              // row kernels: 2 auto (default), 0 pipelined, 1 high-occupancy (env DECMG_KERNEL)
     decmg_gpu::Timing timing;
     std::string err;

@@ -266,6 +266,38 @@ struct Driver {
         const double R = nrhs;
         const double* x = xcur(L);
         const double* b = bptr(k);
+        if (c->rr_window && L.rr_crows && tpr <= 8 && !c->fuse_rr) {
+            // residual kept in a shared-memory window, restriction in the same pass
+            const double bytes = 12.0 * L.nnzR + 4.0 * (C.nv + 1) + 12.0 * L.nnzL + 4.0 * (L.nv + 1) +
+                                 16.0 * L.nv * R + 8.0 * C.nv * R;
+            const int cls = k == 0 ? kRestrict : kCoarseLevels;
+            const int* zr = c->dirichlet ? C.bd_i : nullptr;
+            Status st;
+            DISPATCH_BP(key, {
+                auto go = [&](auto wl, auto wr) {
+                    constexpr int WL = decltype(wl)::value, WRr = decltype(wr)::value;
+                    using G = PipeGeom<BP, RPT, WL>;
+                    auto kern = k_res_restrict<BP, RPT, WL, WRr>;
+                    const size_t smem = static_cast<size_t>(kPipeStages) * G::STAGE_BYTES +
+                                        static_cast<size_t>(kRRWindow) * G::ROWS * BP * sizeof(double);
+                    static bool attr = false;
+                    if (!attr) {
+                        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+                        attr = true;
+                    }
+                    const int ntiles = (L.nv + G::ROWS - 1) / G::ROWS;
+                    const int g = ntiles < 2 * c->num_sms ? ntiles : 2 * c->num_sms;
+                    RRArgs a{ntiles, nrhs, L.nv, L.Le_ci, L.Le_v, L.Le_row, x, b, L.Re_ci, L.Re_v, L.rr_crows,
+                             L.rr_gptr, L.rr_ngran, C.b, zr, c->pf};
+                    return launch(c, cls, bytes, [&] { kern<<<g, kPipeThreads, smem, c->stream>>>(a); });
+                };
+                using I7 = std::integral_constant<int, 7>;
+                using I8 = std::integral_constant<int, 8>;
+                if (L.Le_w == 7) st = L.Re_w == 7 ? go(I7{}, I7{}) : go(I7{}, I8{});
+                else st = L.Re_w == 7 ? go(I8{}, I7{}) : go(I8{}, I8{});
+            })
+            return st;
+        }
         if (c->fuse_rr && L.Le_ci && L.Re_ci && tpr <= 8) {
             // one pass: every R row recomputes the fine residuals it needs
             const double bytes = 12.0 * L.nnzR + 4.0 * (C.nv + 1) + 12.0 * L.nnzL + 4.0 * (L.nv + 1) +

@@ -535,6 +535,19 @@ __global__ void k_gs_keys(int n, const int* __restrict__ ord, const int* __restr
     q[r] = static_cast<int>(r);
 }
 
+// Coarse rows by the 4-row granule of their first (renumbered) R column.
+__global__ void k_rr_count(int nc, const int* __restrict__ rp, const int* __restrict__ ci, int* __restrict__ cnt) {
+    const int64_t q = gtid();
+    if (q < nc) atomicAdd(&cnt[ci[rp[q]] / 4], 1);
+}
+__global__ void k_rr_fill(int nc, const int* __restrict__ rp, const int* __restrict__ ci,
+                          const int* __restrict__ gptr, int* __restrict__ cursor, int* __restrict__ crows) {
+    const int64_t q = gtid();
+    if (q >= nc) return;
+    const int g = ci[rp[q]] / 4;
+    crows[gptr[g] + atomicAdd(&cursor[g], 1)] = static_cast<int>(q);
+}
+
 __global__ void k_invert(int n, const int* __restrict__ ord, int* __restrict__ inv) {
     const int64_t q = gtid();
     if (q < n) inv[ord[q]] = static_cast<int>(q);
@@ -1003,6 +1016,21 @@ Status build_orders(decmg_gpu_ctx* c) {
                          &m.Re_w));
         DG_TRY(build_sweep2(c, m));
         DG_TRY(build_gs_schedule(c, m));
+        if (m.Le_ci && m.Re_ci) {  // fused residual + restriction lookup
+            TmpPool tp(c->stream);
+            const int ng = (m.nv + 3) / 4;
+            int *cnt, *cursor;
+            DG_TRY(tp.get(&cnt, ng + 1));
+            DG_TRY(tp.get(&cursor, ng + 1));
+            DG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * (ng + 1), c->stream));
+            DG_CUDA(cudaMemsetAsync(cursor, 0, sizeof(int) * (ng + 1), c->stream));
+            LAUNCH(4, cm.nv, k_rr_count, cm.nv, m.Ro_rp, m.Ro_ci, cnt);
+            DG_TRY(dalloc(c, &m.rr_gptr, ng + 1));
+            DG_TRY(exclusive_scan(c, cnt, m.rr_gptr, ng));
+            DG_TRY(dalloc(c, &m.rr_crows, cm.nv));
+            LAUNCH(4, cm.nv, k_rr_fill, cm.nv, m.Ro_rp, m.Ro_ci, m.rr_gptr, cursor, m.rr_crows);
+            m.rr_ngran = ng;
+        }
         if (m.Pe_ci && !m.Le_row) {  // P rows share L's row ids
             m.Pe_ci = nullptr;
             m.Pe_v = nullptr;

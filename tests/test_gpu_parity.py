@@ -387,8 +387,8 @@ def test_setup_errors_match_reference_messages():
         d.MultigridHierarchy.from_base((Q, np.array([[0, 1, 2]])), 0)
 
 
-@pytest.mark.parametrize("env", [{"DECMG_FUSE_RR": "1"}, {"DECMG_KERNEL": "ell"}, {"DECMG_SWEEP2": "1"},
-                                 {"DECMG_PF": "0"}, {"DECMG_RPT": "2"}])
+@pytest.mark.parametrize("env", [{"DECMG_FUSE_RR": "1"}, {"DECMG_RR_WINDOW": "1"}, {"DECMG_KERNEL": "ell"},
+                                 {"DECMG_SWEEP2": "1"}, {"DECMG_PF": "0"}, {"DECMG_RPT": "2"}])
 @pytest.mark.parametrize("base,nsub,dirichlet,nrhs", [("ico", 6, False, 16), ("square", 6, True, 1)])
 def test_kernel_variants_bitwise(monkeypatch, env, base, nsub, dirichlet, nrhs):
     """Every opt-in kernel variant (fused residual-restriction, high-occupancy

@@ -33,3 +33,20 @@ for k in (0, 56, 224, 1024, 4096, 16384, 65536):
 dref = np.abs(ci - rows)
 for k in (1024, 65536):
     print(f"  neighbour refs within +-{k:6d} reference rows: {np.mean(dref <= k):.4f}")
+
+# restriction rows: R row of coarse vertex i gathers the fine residual at its
+# copy (reference id i) and at the midpoints around it; distance of those
+# columns from the copy's internal row (the window a fused residual +
+# restriction pass would need)
+Rrp = h.export(0, "R_row_ptr").astype(np.int64)
+Rci = h.export(0, "R_col_idx").astype(np.int64)
+nc = Rrp.size - 1
+crow = np.repeat(np.arange(nc), np.diff(Rrp))
+dR = pos[Rci] - pos[crow]
+for lo, hi in ((-56, 56), (-112, 56), (-112, 112), (-224, 112), (-224, 224)):
+    print(f"  R entries with column within [{lo}, +{hi}] rows of the copy: {np.mean((dR >= lo) & (dR <= hi)):.4f}")
+rows_ok = np.zeros(nc, bool)
+for lo, hi in ((-112, 56), (-224, 112)):
+    ok = (dR >= lo) & (dR <= hi)
+    allok = np.minimum.reduceat(ok.astype(np.int8), Rrp[:-1]) == 1
+    print(f"  R rows with every column within [{lo}, +{hi}]: {np.mean(allok):.4f}")
