@@ -322,6 +322,87 @@ static int binary_subdivide(const mesh_t* c, mesh_t* f, int project) {
     return rc;
 }
 
+/* subdivide_nary with n = 3, "cubic" (proj/src/subdivision.cpp:12-110,
+ * 116-120): copies; two points per coarse edge at p_s*(1-t_k) + p_t*t_k,
+ * t_k = k/3 (k = 1, 2; ids nv + 2e + k - 1); one point per triangle at
+ * (p0*b0 + p1*b1) + p2*b2 with b1 = b2 = 1/3, b0 = 1 - b1 - b2 (id
+ * nv + 2ne + t); nine children per parent over the barycentric lattice
+ * (lattice_vertex, 63-87; loop 89-103). project != 0: every new point scaled
+ * by 1.0/|p| (extension x2 for the icosphere). Also returns the map columns
+ * (fine vertex -> up to 3 (coarse vertex, weight) pairs, unsorted) for
+ * build_transfers_nary. */
+typedef struct { int n; int v[3]; double w[3]; } mcol_t;
+
+static int cubic_lattice(const mesh_t* c, int t, int i, int j) {
+    const int n = 3, nv = c->nv;
+    const int v0 = c->corners[3 * t], v1 = c->corners[3 * t + 1], v2 = c->corners[3 * t + 2];
+    const int k0 = n - i - j;
+    if (i == 0 && j == 0) return v0;
+    if (k0 == 0 && j == 0) return v1;
+    if (k0 == 0 && i == 0) return v2;
+    int a, b, k;
+    if (j == 0) { a = v0; b = v1; k = i; }
+    else if (i == 0) { a = v0; b = v2; k = j; }
+    else if (k0 == 0) { a = v1; b = v2; k = j; }
+    else return nv + 2 * c->ne + t;  /* the single interior point of n = 3 */
+    const int e = find_edge(c, a, b);
+    const int step = c->edges[2 * e] == a ? k : n - k;
+    return nv + e * 2 + (step - 1);
+}
+
+static int cubic_subdivide(const mesh_t* c, mesh_t* f, int project, mcol_t** cols_out) {
+    const int nv = c->nv, ne = c->ne, nt = c->nt;
+    const int fnv = nv + 2 * ne + nt;
+    double* pos = NEW(double, 3 * (size_t)fnv);
+    mcol_t* cols = NEW(mcol_t, fnv);
+    memcpy(pos, c->pos, (size_t)nv * 3 * sizeof(double));
+    for (int v = 0; v < nv; ++v) { cols[v].n = 1; cols[v].v[0] = v; cols[v].w[0] = 1.0; }
+    for (int e = 0; e < ne; ++e) {
+        const int s = c->edges[2 * e], t = c->edges[2 * e + 1];
+        const v3 ps = v3_at(c->pos, s), pt = v3_at(c->pos, t);
+        for (int k = 1; k <= 2; ++k) {
+            const double tk = (double)k / 3;
+            v3 p = v3_add(v3_mul(ps, 1.0 - tk), v3_mul(pt, tk));
+            if (project) p = v3_mul(p, 1.0 / v3_norm(p));
+            const int j = nv + 2 * e + (k - 1);
+            pos[3 * j] = p.x; pos[3 * j + 1] = p.y; pos[3 * j + 2] = p.z;
+            cols[j].n = 2; cols[j].v[0] = s; cols[j].w[0] = 1.0 - tk; cols[j].v[1] = t; cols[j].w[1] = tk;
+        }
+    }
+    for (int t = 0; t < nt; ++t) {
+        const int v0 = c->corners[3 * t], v1 = c->corners[3 * t + 1], v2 = c->corners[3 * t + 2];
+        const double b1 = 1.0 / 3, b2 = 1.0 / 3, b0 = 1.0 - b1 - b2;
+        v3 p = v3_add(v3_add(v3_mul(v3_at(c->pos, v0), b0), v3_mul(v3_at(c->pos, v1), b1)),
+                      v3_mul(v3_at(c->pos, v2), b2));
+        if (project) p = v3_mul(p, 1.0 / v3_norm(p));
+        const int j = nv + 2 * ne + t;
+        pos[3 * j] = p.x; pos[3 * j + 1] = p.y; pos[3 * j + 2] = p.z;
+        cols[j].n = 3;
+        cols[j].v[0] = v0; cols[j].w[0] = b0;
+        cols[j].v[1] = v1; cols[j].w[1] = b1;
+        cols[j].v[2] = v2; cols[j].w[2] = b2;
+    }
+    int* tri = NEW(int, 27 * (size_t)nt);
+    int q = 0;
+    for (int t = 0; t < nt; ++t)
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; i + j < 3; ++j) {
+                tri[q++] = cubic_lattice(c, t, i, j);
+                tri[q++] = cubic_lattice(c, t, i + 1, j);
+                tri[q++] = cubic_lattice(c, t, i, j + 1);
+                if (i + j < 2) {
+                    tri[q++] = cubic_lattice(c, t, i + 1, j);
+                    tri[q++] = cubic_lattice(c, t, i + 1, j + 1);
+                    tri[q++] = cubic_lattice(c, t, i, j + 1);
+                }
+            }
+    int rc = mesh_from_triangles(f, pos, fnv, tri, 9 * nt);
+    free(tri);
+    if (rc) { free(cols); return rc; }
+    *cols_out = cols;
+    return 0;
+}
+
 /* ---------------------------------------------------------------- level -- */
 typedef struct {
     mesh_t m;
@@ -478,6 +559,71 @@ static void build_transfers(level_t* fine, const level_t* coarse) {
     fine->R_rp[nvc] = (int)k;
 }
 
+/* P = M(f)^T and R = rownormalize(M(f)) from general map columns
+ * (GeometricMap::make, geometric_map.cpp:18-42: drop |w| <= 1e-12, renormalise
+ * by the column's sequential sum when |sum - 1| <= 1e-9, sort by vertex;
+ * matrix / transposed, sparse.cpp:90-115; restriction_matrix 205-223: row sums
+ * accumulated over fine columns in ascending order, inv = 1.0/sum,
+ * R_ij = M_ij * inv). */
+static void build_transfers_nary(level_t* fine, const level_t* coarse, mcol_t* cols) {
+    const int nvc = coarse->m.nv, nvf = fine->m.nv;
+    int64_t nnz = 0;
+    for (int j = 0; j < nvf; ++j) {
+        mcol_t* c = &cols[j];
+        mcol_t k;
+        k.n = 0;
+        double sum = 0.0;
+        for (int a = 0; a < c->n; ++a) {
+            if (fabs(c->w[a]) <= 1e-12) continue;
+            k.v[k.n] = c->v[a]; k.w[k.n] = c->w[a]; ++k.n;
+            sum += c->w[a];
+        }
+        if (fabs(sum - 1.0) <= 1e-9 && sum != 0.0)
+            for (int a = 0; a < k.n; ++a) k.w[a] /= sum;
+        for (int a = 1; a < k.n; ++a)  /* sort by (vertex, weight) */
+            for (int b = a; b > 0 && (k.v[b] < k.v[b - 1] || (k.v[b] == k.v[b - 1] && k.w[b] < k.w[b - 1])); --b) {
+                int tv = k.v[b]; k.v[b] = k.v[b - 1]; k.v[b - 1] = tv;
+                double tw = k.w[b]; k.w[b] = k.w[b - 1]; k.w[b - 1] = tw;
+            }
+        *c = k;
+        nnz += k.n;
+    }
+    fine->nnzP = fine->nnzR = nnz;
+    fine->P_rp = NEW(int, nvf + 1);
+    fine->P_ci = NEW(int, nnz);
+    fine->P_v = NEW(double, nnz);
+    int64_t q = 0;
+    for (int j = 0; j < nvf; ++j) {
+        fine->P_rp[j] = (int)q;
+        for (int a = 0; a < cols[j].n; ++a) { fine->P_ci[q] = cols[j].v[a]; fine->P_v[q] = cols[j].w[a]; ++q; }
+    }
+    fine->P_rp[nvf] = (int)q;
+    /* R: rows = coarse vertices, columns (fine j) ascending */
+    fine->R_rp = NEW(int, nvc + 1);
+    fine->R_ci = NEW(int, nnz);
+    fine->R_v = NEW(double, nnz);
+    int* cnt = NEW(int, nvc + 1);
+    memset(cnt, 0, sizeof(int) * (nvc + 1));
+    for (int64_t e = 0; e < nnz; ++e) ++cnt[fine->P_ci[e] + 1];
+    for (int i = 0; i < nvc; ++i) cnt[i + 1] += cnt[i];
+    memcpy(fine->R_rp, cnt, sizeof(int) * (nvc + 1));
+    double* rs = NEW(double, nvc);
+    for (int i = 0; i < nvc; ++i) rs[i] = 0.0;
+    for (int j = 0; j < nvf; ++j)
+        for (int a = fine->P_rp[j]; a < fine->P_rp[j + 1]; ++a) {
+            const int i = fine->P_ci[a];
+            fine->R_ci[cnt[i]] = j;
+            fine->R_v[cnt[i]] = fine->P_v[a];
+            ++cnt[i];
+            rs[i] += fine->P_v[a];
+        }
+    for (int i = 0; i < nvc; ++i) {
+        const double inv = 1.0 / rs[i];
+        for (int a = fine->R_rp[i]; a < fine->R_rp[i + 1]; ++a) fine->R_v[a] = fine->R_v[a] * inv;
+    }
+    free(cnt); free(rs);
+}
+
 static void level_free(level_t* lv) {
     mesh_free(&lv->m);
     free(lv->area); free(lv->bd); free(lv->L_rp); free(lv->L_ci); free(lv->L_v); free(lv->diag);
@@ -499,7 +645,15 @@ orc_hier* orc_build(const char* base, int nsub, int dirichlet) {
     h->L = nsub + 1;
     h->dirichlet = dirichlet;
     h->lv = (level_t*)calloc((size_t)h->L, sizeof(level_t));
-    int project = 0, rc;
+    int project = 0, rc, cubic = 0;
+    char spec[256];
+    snprintf(spec, sizeof spec, "%s", base);
+    const size_t sl = strlen(spec);
+    if (sl > 6 && strcmp(spec + sl - 6, "+cubic") == 0) {  /* SubdivisionScheme::Cubic */
+        cubic = 1;
+        spec[sl - 6] = 0;
+    }
+    base = spec;
     mesh_t* b = &h->lv[h->L - 1].m;
     if (strcmp(base, "square") == 0) {
         rc = base_grid(b, 1, 1, 1.0, 1.0);
@@ -520,11 +674,22 @@ orc_hier* orc_build(const char* base, int nsub, int dirichlet) {
         return NULL;
     }
     if (rc) { orc_free(h); return NULL; }
-    for (int k = h->L - 2; k >= 0; --k)
-        if (binary_subdivide(&h->lv[k + 1].m, &h->lv[k].m, project)) { orc_free(h); return NULL; }
-    for (int k = 0; k < h->L; ++k)
-        if (assemble_level(&h->lv[k], dirichlet)) { orc_free(h); return NULL; }
-    for (int k = 0; k + 1 < h->L; ++k) build_transfers(&h->lv[k], &h->lv[k + 1]);
+    mcol_t** cols = cubic ? (mcol_t**)calloc((size_t)h->L, sizeof(mcol_t*)) : NULL;
+    for (int k = h->L - 2; k >= 0; --k) {
+        rc = cubic ? cubic_subdivide(&h->lv[k + 1].m, &h->lv[k].m, project, &cols[k])
+                   : binary_subdivide(&h->lv[k + 1].m, &h->lv[k].m, project);
+        if (rc) break;
+    }
+    for (int k = 0; !rc && k < h->L; ++k) rc = assemble_level(&h->lv[k], dirichlet);
+    for (int k = 0; !rc && k + 1 < h->L; ++k) {
+        if (cubic) build_transfers_nary(&h->lv[k], &h->lv[k + 1], cols[k]);
+        else build_transfers(&h->lv[k], &h->lv[k + 1]);
+    }
+    if (cols) {
+        for (int k = 0; k < h->L; ++k) free(cols[k]);
+        free(cols);
+    }
+    if (rc) { orc_free(h); return NULL; }
     const level_t* cl = &h->lv[h->L - 1];
     h->wtot_coarse = 0.0;
     for (int i = 0; i < cl->m.nv; ++i) h->wtot_coarse += cl->area[i];

@@ -84,11 +84,11 @@ std::shared_ptr<EmbeddedComplex2D> ico_base() {
     return EmbeddedComplex2D::from_triangles(std::move(pos), tris);
 }
 
-// Projected binary subdivision: the reference's binary_subdivide, then every
-// new edge-midpoint vertex is pushed to the unit sphere as p * (1.0 / |p|);
-// copied vertices keep their bits. Map columns are unchanged (1/2, 1/2).
-SubdivisionResult projected_subdivide(const std::shared_ptr<const EmbeddedComplex2D>& c) {
-    SubdivisionResult s = binary_subdivide(c);
+// Projected subdivision: the reference's binary (or cubic) subdivide, then
+// every new vertex is pushed to the unit sphere as p * (1.0 / |p|); copied
+// vertices keep their bits. Map columns are unchanged.
+SubdivisionResult projected_subdivide(const std::shared_ptr<const EmbeddedComplex2D>& c, bool cubic = false) {
+    SubdivisionResult s = cubic ? cubic_subdivide(c) : binary_subdivide(c);
     const int nvc = c->num_vertices();
     std::vector<Vec3> pos = s.fine->positions;
     for (std::size_t v = nvc; v < pos.size(); ++v) {
@@ -109,10 +109,18 @@ SubdivisionResult projected_subdivide(const std::shared_ptr<const EmbeddedComple
 struct Case {
     std::shared_ptr<EmbeddedComplex2D> base;
     bool project = false;
+    bool cubic = false;  // SubdivisionScheme::Cubic (1 -> 9) instead of Binary
 };
 
-Case make_case(const std::string& spec) {
+// <base>[+cubic], base one of square | ico | grid:nx:ny:lx:ly | equi:rows:cols:side
+Case make_case(const std::string& spec_in) {
     Case c;
+    std::string spec = spec_in;
+    const std::string suffix = "+cubic";
+    if (spec.size() > suffix.size() && spec.compare(spec.size() - suffix.size(), suffix.size(), suffix) == 0) {
+        c.cubic = true;
+        spec = spec.substr(0, spec.size() - suffix.size());
+    }
     if (spec == "square") {
         c.base = make_triangulated_grid(1, 1, 1.0, 1.0);
     } else if (spec == "ico") {
@@ -138,11 +146,12 @@ Case make_case(const std::string& spec) {
 
 std::vector<SubdivisionResult> tower_of(const Case& c, int k) {
     if (k == 0) return {};
-    if (!c.project) return subdivision_tower(c.base, SubdivisionScheme::Binary, k);
+    if (!c.project)
+        return subdivision_tower(c.base, c.cubic ? SubdivisionScheme::Cubic : SubdivisionScheme::Binary, k);
     std::vector<SubdivisionResult> chain;
     std::shared_ptr<const EmbeddedComplex2D> cur = c.base;
     for (int i = 0; i < k; ++i) {
-        chain.push_back(projected_subdivide(cur));
+        chain.push_back(projected_subdivide(cur, c.cubic));
         cur = chain.back().fine;
     }
     std::reverse(chain.begin(), chain.end());

@@ -33,6 +33,11 @@ STRUCTURE = [
     ("struct_ico_4", ["structure", "ico", "4", "neumann"]),
     ("struct_ico_6", ["structure", "ico", "6", "neumann"]),
     ("struct_equi_4_8_3", ["structure", "equi:4:8:1.0", "3", "neumann"]),
+    # SubdivisionScheme::Cubic (subdivision.cpp:116-120), "<base>+cubic"
+    ("struct_square_cubic_2_full", ["structure", "square+cubic", "2", "neumann", "full"]),
+    ("struct_square_cubic_3_dirichlet", ["structure", "square+cubic", "3", "dirichlet"]),
+    ("struct_ico_cubic_3", ["structure", "ico+cubic", "3", "neumann"]),
+    ("struct_equi_cubic_2", ["structure", "equi:4:8:1.0+cubic", "2", "neumann"]),
 ]
 CYCLES = [
     ("cycles_square_4_dirichlet_sinsin", ["cycles", "square", "4", "dirichlet", "sinsin", "0", "12"]),
@@ -45,6 +50,9 @@ CYCLES = [
     ("cycles_ico_5_ylm_gs", ["cycles", "ico", "5", "neumann", "ylm", "2", "5", "gs"]),
     ("cycles_square_4_dirichlet_sinsin_gs", ["cycles", "square", "4", "dirichlet", "sinsin", "0", "8", "gs"]),
     ("cycles_equi_4_8_3_lr_sgs", ["cycles", "equi:4:8:1.0", "3", "neumann", "lr", "3", "6", "sgs"]),
+    ("cycles_square_cubic_3_dirichlet_sinsin", ["cycles", "square+cubic", "3", "dirichlet", "sinsin", "0", "8"]),
+    ("cycles_ico_cubic_3_uniform", ["cycles", "ico+cubic", "3", "neumann", "uniform", "1", "8"]),
+    ("cycles_ico_cubic_2_ylm_gs", ["cycles", "ico+cubic", "2", "neumann", "ylm", "2", "5", "gs"]),
 ]
 SOLVES = [
     # BASELINE configs 1-3 (config 3 takes ~30 s of reference setup)
@@ -55,6 +63,8 @@ SOLVES = [
     ("solve_square_6_uniform", ["solve", "square", "6", "neumann", "uniform", "5", "1e-8", "200"]),
     ("solve_config2_gs", ["solve", "ico", "6", "neumann", "ylm", "1", "1e-8", "200", "gs"]),
     ("solve_config1_sgs", ["solve", "square", "4", "dirichlet", "sinsin", "0", "1e-8", "200", "sgs"]),
+    ("solve_ico_cubic_3_ylm", ["solve", "ico+cubic", "3", "neumann", "ylm", "1", "1e-8", "300"]),
+    ("solve_square_cubic_4_uniform", ["solve", "square+cubic", "4", "neumann", "uniform", "5", "1e-8", "300"]),
 ]
 PCG = [
     # gmg_preconditioned_cg (solvers.cpp:118-130): <rhs> <seed> <V|W> <pre> <post> <cycles> <tol> <maxit> [smoother]
