@@ -50,6 +50,7 @@ enum {
 /* creation flags */
 #define DECMG_PROJECT_SPHERE 1u /* push new midpoints to the unit sphere (x2)   */
 #define DECMG_DIRICHLET 2u      /* identity rows on boundary vertices (x1)      */
+#define DECMG_CUBIC 4u          /* SubdivisionScheme::Cubic (1 -> 9, subdivision.cpp:116-120) instead of Binary */
 
 typedef struct {
     int device;   /* CUDA device ordinal                                    */

@@ -22,6 +22,7 @@ DECMG_OOM = 5
 
 DECMG_PROJECT_SPHERE = 1
 DECMG_DIRICHLET = 2
+DECMG_CUBIC = 4
 
 
 class DecmgError(RuntimeError):

@@ -106,7 +106,185 @@ __global__ void k_sub_tris(int ntc, int nvc, const int* __restrict__ corners_c,
     o[9] = m01; o[10] = v1;  o[11] = m12;
 }
 
-// ------------------------------------------------------ from_triangles -----
+// subdivide_nary n = 3, "cubic" (proj/src/subdivision.cpp:12-110,116-120):
+// copies; points k = 1, 2 of coarse edge e at p_s*(1-t_k) + p_t*t_k, t_k = k/3
+// (ids nvc + 2e + k - 1); the interior point of triangle t at
+// (p0*b0 + p1*b1) + p2*b2, b1 = b2 = 1/3, b0 = (1 - b1) - b2 (id nvc + 2nec + t).
+// project: every new point scaled by 1.0/|p| (extension x2).
+__global__ void k_sub_pos3(int nvc, int nec, int ntc, const double* __restrict__ posc,
+                           const int* __restrict__ edges_c, const int* __restrict__ corners_c,
+                           double* __restrict__ posf, int project) {
+    const int64_t j = gtid();
+    const int64_t ne2 = 2 * static_cast<int64_t>(nec);
+    if (j >= nvc + ne2 + ntc) return;
+    if (j < nvc) {
+        st3(posf, j, ld3(posc, j));
+        return;
+    }
+    V3 p;
+    if (j < nvc + ne2) {
+        const int e = static_cast<int>((j - nvc) / 2), k = static_cast<int>((j - nvc) % 2) + 1;
+        const V3 ps = ld3(posc, edges_c[2 * e]), pt = ld3(posc, edges_c[2 * e + 1]);
+        const double tk = __ddiv_rn(static_cast<double>(k), 3.0);
+        p = add(mul(ps, __dsub_rn(1.0, tk)), mul(pt, tk));
+    } else {
+        const int t = static_cast<int>(j - nvc - ne2);
+        const double b1 = __ddiv_rn(1.0, 3.0), b2 = b1, b0 = __dsub_rn(__dsub_rn(1.0, b1), b2);
+        p = add(add(mul(ld3(posc, corners_c[3 * t]), b0), mul(ld3(posc, corners_c[3 * t + 1]), b1)),
+                mul(ld3(posc, corners_c[3 * t + 2]), b2));
+    }
+    if (project) {
+        const double inv = __ddiv_rn(1.0, norm(p));
+        p = mul(p, inv);
+    }
+    st3(posf, j, p);
+}
+
+// lattice_vertex (subdivision.cpp:63-87) for n = 3; the parent triangle
+// stores e(v1,v2), e(v0,v2), e(v0,v1) (mesh.cpp:149-154)
+__device__ int lattice3(int nvc, int nec, int t, int v0, int v1, int v2, const int* tris_c, const int* edges_c, int i,
+                        int j) {
+    const int k0 = 3 - i - j;
+    if (i == 0 && j == 0) return v0;
+    if (k0 == 0 && j == 0) return v1;
+    if (k0 == 0 && i == 0) return v2;
+    int a, e, k;
+    if (j == 0) { a = v0; e = tris_c[3 * t + 2]; k = i; }
+    else if (i == 0) { a = v0; e = tris_c[3 * t + 1]; k = j; }
+    else if (k0 == 0) { a = v1; e = tris_c[3 * t]; k = j; }
+    else return nvc + 2 * nec + t;
+    const int step = edges_c[2 * e] == a ? k : 3 - k;
+    return nvc + e * 2 + (step - 1);
+}
+
+// nine children per parent in the lattice loop order (subdivision.cpp:89-103)
+__global__ void k_sub_tris3(int ntc, int nvc, int nec, const int* __restrict__ corners_c,
+                            const int* __restrict__ tris_c, const int* __restrict__ edges_c,
+                            int* __restrict__ corners_f) {
+    const int64_t t = gtid();
+    if (t >= ntc) return;
+    const int v0 = corners_c[3 * t], v1 = corners_c[3 * t + 1], v2 = corners_c[3 * t + 2];
+    int* o = corners_f + 27 * t;
+    int q = 0;
+    auto L = [&](int i, int j) { return lattice3(nvc, nec, static_cast<int>(t), v0, v1, v2, tris_c, edges_c, i, j); };
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; i + j < 3; ++j) {
+            o[q++] = L(i, j);
+            o[q++] = L(i + 1, j);
+            o[q++] = L(i, j + 1);
+            if (i + j < 2) {
+                o[q++] = L(i + 1, j);
+                o[q++] = L(i + 1, j + 1);
+                o[q++] = L(i, j + 1);
+            }
+        }
+}
+
+// Map-column weights of the cubic points after GeometricMap::make
+// (geometric_map.cpp:18-42): renormalised by the column's sequential sum when
+// |sum - 1| <= 1e-9 (the sums here are 1.0, so the weights keep their bits).
+__device__ void cubic_edge_w(int k, double* ws, double* wt) {
+    const double tk = __ddiv_rn(static_cast<double>(k), 3.0);
+    double a = __dsub_rn(1.0, tk), b = tk;
+    const double sum = __dadd_rn(__dadd_rn(0.0, a), b);
+    if (fabs(__dsub_rn(sum, 1.0)) <= 1e-9 && sum != 0.0) {
+        a = __ddiv_rn(a, sum);
+        b = __ddiv_rn(b, sum);
+    }
+    *ws = a;
+    *wt = b;
+}
+__device__ void cubic_face_w(double* w) {
+    const double b1 = __ddiv_rn(1.0, 3.0), b2 = b1, b0 = __dsub_rn(__dsub_rn(1.0, b1), b2);
+    w[0] = b0; w[1] = b1; w[2] = b2;
+    const double sum = __dadd_rn(__dadd_rn(__dadd_rn(0.0, b0), b1), b2);
+    if (fabs(__dsub_rn(sum, 1.0)) <= 1e-9 && sum != 0.0)
+        for (int a = 0; a < 3; ++a) w[a] = __ddiv_rn(w[a], sum);
+}
+
+// P = M(f)^T for the cubic map: rows sorted by coarse column (and weight)
+__global__ void k_P_fill3(int nvf, int nvc, int nec, const int* __restrict__ edges_c,
+                          const int* __restrict__ corners_c, int* __restrict__ rp, int* __restrict__ ci,
+                          double* __restrict__ v) {
+    const int64_t j = gtid();
+    if (j > nvf) return;
+    const int64_t ne2 = 2 * static_cast<int64_t>(nec);
+    const int64_t r = j < nvc ? j : (j < nvc + ne2 ? nvc + 2 * (j - nvc) : nvc + 2 * ne2 + 3 * (j - nvc - ne2));
+    rp[j] = static_cast<int>(r);
+    if (j == nvf) return;
+    if (j < nvc) {
+        ci[r] = static_cast<int>(j);
+        v[r] = 1.0;
+    } else if (j < nvc + ne2) {
+        const int e = static_cast<int>((j - nvc) / 2), k = static_cast<int>((j - nvc) % 2) + 1;
+        double ws, wt;
+        cubic_edge_w(k, &ws, &wt);
+        ci[r] = edges_c[2 * e];  // src < tgt
+        v[r] = ws;
+        ci[r + 1] = edges_c[2 * e + 1];
+        v[r + 1] = wt;
+    } else {
+        const int t = static_cast<int>(j - nvc - ne2);
+        double w[3];
+        cubic_face_w(w);
+        int vv[3] = {corners_c[3 * t], corners_c[3 * t + 1], corners_c[3 * t + 2]};
+        for (int a = 1; a < 3; ++a)  // sort (vertex, weight) pairs
+            for (int b = a; b > 0 && (vv[b] < vv[b - 1] || (vv[b] == vv[b - 1] && w[b] < w[b - 1])); --b) {
+                const int tv = vv[b]; vv[b] = vv[b - 1]; vv[b - 1] = tv;
+                const double tw = w[b]; w[b] = w[b - 1]; w[b - 1] = tw;
+            }
+        for (int a = 0; a < 3; ++a) {
+            ci[r + a] = vv[a];
+            v[r + a] = w[a];
+        }
+    }
+}
+
+// R = rownormalize(M(f)) for the cubic map (geometric_map.cpp:205-223): row i
+// = its copy, the two points of each incident edge (ascending edge), the
+// interior point of each incident triangle (ascending triangle) -- ascending
+// fine id -- with the row sum accumulated in that order.
+__global__ void k_R_fill3(int nvc, int nec, const int* __restrict__ ve_ptr, const int* __restrict__ ve,
+                          const int* __restrict__ vt_ptr, const int* __restrict__ vt,
+                          const int* __restrict__ edges_c, int* __restrict__ rp, int* __restrict__ ci,
+                          double* __restrict__ v) {
+    const int64_t i = gtid();
+    if (i > nvc) return;
+    const int r0 = static_cast<int>(i) + 2 * ve_ptr[i] + vt_ptr[i];
+    rp[i] = r0;
+    if (i == nvc) return;
+    double fw[3];
+    cubic_face_w(fw);
+    double rs = __dadd_rn(0.0, 1.0);
+    for (int q = ve_ptr[i]; q < ve_ptr[i + 1]; ++q) {
+        const int e = ve[q];
+        for (int k = 1; k <= 2; ++k) {
+            double ws, wt;
+            cubic_edge_w(k, &ws, &wt);
+            rs = __dadd_rn(rs, edges_c[2 * e] == i ? ws : wt);
+        }
+    }
+    for (int q = vt_ptr[i]; q < vt_ptr[i + 1]; ++q) rs = __dadd_rn(rs, fw[vt[q] % 3]);
+    const double inv = __ddiv_rn(1.0, rs);
+    int k = r0;
+    ci[k] = static_cast<int>(i);
+    v[k++] = __dmul_rn(1.0, inv);
+    for (int q = ve_ptr[i]; q < ve_ptr[i + 1]; ++q) {
+        const int e = ve[q];
+        for (int kk = 1; kk <= 2; ++kk) {
+            double ws, wt;
+            cubic_edge_w(kk, &ws, &wt);
+            ci[k] = nvc + 2 * e + (kk - 1);
+            v[k++] = __dmul_rn(edges_c[2 * e] == i ? ws : wt, inv);
+        }
+    }
+    for (int q = vt_ptr[i]; q < vt_ptr[i + 1]; ++q) {
+        ci[k] = nvc + 2 * nec + vt[q] / 3;
+        v[k++] = __dmul_rn(fw[vt[q] % 3], inv);
+    }
+}
+
+// ------------------------------------------------------ from_triangles -----// ------------------------------------------------------ from_triangles -----
 __global__ void k_check_triples(int nt, int nv, const int* __restrict__ c, int* bad) {
     const int64_t t = gtid();
     if (t >= nt) return;
@@ -1057,13 +1235,20 @@ Status build_from_base(decmg_gpu_ctx* c, const double* hpos, int nv, const int* 
                        int nsub, unsigned flags) {
     if (nv < 3 || nt < 1 || nsub < 0) return Status::Err(DECMG_INVALID_ARGUMENT, "create_from_base: bad sizes");
     const int L = nsub + 1;
+    const bool cubic = (flags & DECMG_CUBIC) != 0;
     // size guard: every count must stay inside int32 (reference uses int)
     {
         int64_t v = nv, t = nt, e = 3 * static_cast<int64_t>(nt);
         for (int k = 0; k < nsub; ++k) {
-            v = v + e;
-            e = 2 * e + 3 * t;
-            t = 4 * t;
+            if (cubic) {
+                v = v + 2 * e + t;
+                e = 3 * e + 9 * t;
+                t = 9 * t;
+            } else {
+                v = v + e;
+                e = 2 * e + 3 * t;
+                t = 4 * t;
+            }
         }
         if (v + 2 * e > INT32_MAX || 3 * t > INT32_MAX)
             return Status::Err(DECMG_INVALID_ARGUMENT, "create_from_base: mesh exceeds int32 indexing");
@@ -1080,20 +1265,26 @@ Status build_from_base(decmg_gpu_ctx* c, const double* hpos, int nv, const int* 
     DG_TRY(mesh_from_triangles(c, c->lv[L - 1], pos, nv, cor, nt));
     for (int k = L - 2; k >= 0; --k) {
         const Level& cm = c->lv[k + 1];
-        const int fnv = cm.nv + cm.ne, fnt = 4 * cm.nt;
+        const int fnv = cubic ? cm.nv + 2 * cm.ne + cm.nt : cm.nv + cm.ne, fnt = (cubic ? 9 : 4) * cm.nt;
         double* fpos;
         int* fcor;
         DG_TRY(dalloc(c, &fpos, 3 * static_cast<size_t>(fnv)));
         DG_TRY(dalloc(c, &fcor, 3 * static_cast<size_t>(fnt)));
-        LAUNCH(4, fnv, k_sub_pos, cm.nv, cm.ne, cm.pos, cm.edges, fpos, project);
-        LAUNCH(4, cm.nt, k_sub_tris, cm.nt, cm.nv, cm.corners, cm.tris, fcor);
+        if (cubic) {
+            LAUNCH(4, fnv, k_sub_pos3, cm.nv, cm.ne, cm.nt, cm.pos, cm.edges, cm.corners, fpos, project);
+            LAUNCH(4, cm.nt, k_sub_tris3, cm.nt, cm.nv, cm.ne, cm.corners, cm.tris, cm.edges, fcor);
+        } else {
+            LAUNCH(4, fnv, k_sub_pos, cm.nv, cm.ne, cm.pos, cm.edges, fpos, project);
+            LAUNCH(4, cm.nt, k_sub_tris, cm.nt, cm.nv, cm.corners, cm.tris, fcor);
+        }
         DG_TRY(mesh_from_triangles(c, c->lv[k], fpos, fnv, fcor, fnt));
     }
     for (int k = 0; k < L; ++k) DG_TRY(assemble(c, c->lv[k], c->dirichlet));
     for (int k = 0; k + 1 < L; ++k) {
         Level& f = c->lv[k];
         const Level& cm = c->lv[k + 1];
-        f.nnzP = static_cast<int64_t>(cm.nv) + 2 * static_cast<int64_t>(cm.ne);
+        f.nnzP = cubic ? static_cast<int64_t>(cm.nv) + 4 * static_cast<int64_t>(cm.ne) + 3 * static_cast<int64_t>(cm.nt)
+                       : static_cast<int64_t>(cm.nv) + 2 * static_cast<int64_t>(cm.ne);
         f.nnzR = f.nnzP;
         DG_TRY(dalloc(c, &f.P_rp, f.nv + 1));
         DG_TRY(dalloc(c, &f.P_ci, f.nnzP));
@@ -1101,8 +1292,19 @@ Status build_from_base(decmg_gpu_ctx* c, const double* hpos, int nv, const int* 
         DG_TRY(dalloc(c, &f.R_rp, cm.nv + 1));
         DG_TRY(dalloc(c, &f.R_ci, f.nnzR));
         DG_TRY(dalloc(c, &f.R_v, f.nnzR));
-        LAUNCH(4, static_cast<int64_t>(f.nv) + 1, k_P_fill, f.nv, cm.nv, cm.edges, f.P_rp, f.P_ci, f.P_v);
-        LAUNCH(4, static_cast<int64_t>(cm.nv) + 1, k_R_fill, cm.nv, cm.ve_ptr, cm.ve, f.R_rp, f.R_ci, f.R_v);
+        if (cubic) {
+            TmpPool tp(c->stream);
+            int *vt_ptr, *vt;
+            DG_TRY(incidence(c, tp, cm.nt, cm.corners, cm.nv, &vt_ptr, &vt));
+            LAUNCH(4, static_cast<int64_t>(f.nv) + 1, k_P_fill3, f.nv, cm.nv, cm.ne, cm.edges, cm.corners, f.P_rp,
+                   f.P_ci, f.P_v);
+            LAUNCH(4, static_cast<int64_t>(cm.nv) + 1, k_R_fill3, cm.nv, cm.ne, cm.ve_ptr, cm.ve, vt_ptr, vt,
+                   cm.edges, f.R_rp, f.R_ci, f.R_v);
+            DG_CUDA(cudaStreamSynchronize(c->stream));
+        } else {
+            LAUNCH(4, static_cast<int64_t>(f.nv) + 1, k_P_fill, f.nv, cm.nv, cm.edges, f.P_rp, f.P_ci, f.P_v);
+            LAUNCH(4, static_cast<int64_t>(cm.nv) + 1, k_R_fill, cm.nv, cm.ve_ptr, cm.ve, f.R_rp, f.R_ci, f.R_v);
+        }
     }
     // coarsest-level weight total, sequential as PinnedDirectSolver's ctor
     // (proj/src/direct.cpp:44-45)

@@ -214,13 +214,17 @@ class MultigridHierarchy:
     # -- construction ------------------------------------------------------
     @classmethod
     def from_base(cls, base, nsub: int, dirichlet: bool = False, project_sphere: Optional[bool] = None,
-                  device: int = 0, max_nrhs: int = 1) -> "MultigridHierarchy":
-        """build_hierarchy(base, subdivision_tower(base, Binary, nsub)) on the GPU.
+                  device: int = 0, max_nrhs: int = 1, cubic: bool = False) -> "MultigridHierarchy":
+        """build_hierarchy(base, subdivision_tower(base, Binary|Cubic, nsub)) on the GPU.
 
-        base: a spec string for base_mesh() or a (positions, corner_triples) pair.
+        base: a spec string for base_mesh() -- with the suffix "+cubic" for
+        SubdivisionScheme::Cubic, as in the reference harness -- or a
+        (positions, corner_triples) pair.
         """
         lib = _lib.load()
         if isinstance(base, str):
+            if base.endswith("+cubic"):
+                cubic, base = True, base[: -len("+cubic")]
             if project_sphere is None:
                 project_sphere = base == "ico"
             pos, tri = base_mesh(base)
@@ -229,7 +233,8 @@ class MultigridHierarchy:
             project_sphere = bool(project_sphere)
         pos = np.ascontiguousarray(pos, dtype=np.float64)
         tri = np.ascontiguousarray(tri, dtype=np.int32)
-        flags = (_lib.DECMG_PROJECT_SPHERE if project_sphere else 0) | (_lib.DECMG_DIRICHLET if dirichlet else 0)
+        flags = ((_lib.DECMG_PROJECT_SPHERE if project_sphere else 0) | (_lib.DECMG_DIRICHLET if dirichlet else 0)
+                 | (_lib.DECMG_CUBIC if cubic else 0))
         cfg = decmg_gpu_config(device=device, max_nrhs=max_nrhs)
         out = C.c_void_p()
         check(lib.decmg_gpu_create_from_base(_ptr(pos), pos.shape[0], _ptr(tri), tri.shape[0], nsub, flags,

@@ -121,7 +121,8 @@ def test_run_cycle_iterates_bitwise_vs_reference(stem):
 
 
 @pytest.mark.parametrize("stem", ["solve_config1", "solve_config2", "solve_config3", "solve_equi_4_8_3_lr",
-                                  "solve_square_6_uniform", "solve_config2_gs", "solve_config1_sgs"])
+                                  "solve_square_6_uniform", "solve_config2_gs", "solve_config1_sgs",
+                                  "solve_ico_cubic_3_ylm", "solve_square_cubic_4_uniform"])
 def test_gmg_solve_vs_reference(stem):
     """gmg_solve (solvers.cpp:251-279): same cycle count to tol, per-cycle
     residuals within 1e-10 relative (BASELINE configs 1-3; and with the
@@ -455,3 +456,31 @@ def test_partitioned_solve_rejects_gauss_seidel():
     b = np.zeros(dh.context().n())
     with pytest.raises(ValueError, match="only the weighted Jacobi"):
         dh.run_cycle(plan, b)
+
+
+@pytest.mark.parametrize("base,nsub,dirichlet", [("ico+cubic", 4, False), ("square+cubic", 5, True),
+                                                  ("equi:4:8:1.0+cubic", 3, False)])
+def test_cubic_hierarchy_vs_oracle(base, nsub, dirichlet):
+    """SubdivisionScheme::Cubic (1 -> 9) towers up to 66 k vertices: structure,
+    transfers and V(2,2) iterates bit-identical to the oracle (which is pinned
+    to the reference's cubic goldens)."""
+    h = d.MultigridHierarchy.from_base(base, nsub, dirichlet=dirichlet)
+    o = OracleHierarchy(base, nsub, dirichlet)
+    assert h.levels() == o.levels
+    for k in range(h.levels()):
+        assert h.mesh_hash(k) == o.info(k)["hash"]
+        for op, names in EXPORT.items():
+            if op != "L" and k == h.levels() - 1:
+                continue
+            oname = {"L": ("L_rp", "L_ci", "L_v"), "P": ("P_rp", "P_ci", "P_v"), "R": ("R_rp", "R_ci", "R_v")}[op]
+            for gn, on in zip(names, oname):
+                np.testing.assert_array_equal(h.export(k, gn), o.get(k, on))
+    b = o.rhs("sinsin" if dirichlet else "uniform", 9)
+    if not dirichlet:
+        b = o.project(b)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan.cycles = 3
+    res = h.run_cycle(plan, b)
+    ox, oh = o.run_cycles(b, ncycles=3)
+    np.testing.assert_array_equal(res.x, ox)
+    assert np.all(np.abs(res.residual_history - oh) <= RTOL_HIST * oh)
