@@ -180,6 +180,17 @@ DECMG_API int64_t decmg_gpu_launch_count(decmg_gpu_ctx* ctx); /* kernels launche
  * base_mesh spec: "square", "ico", "grid:nx:ny:lx:ly", "equi:rows:cols:side".
  * Query sizes with positions = corners = NULL. */
 DECMG_API int decmg_base_mesh(const char* spec, double* positions, int* nv, int* corners, int* nt);
+
+/* Mesh and operator files (proj/src/mesh_io.cpp:19-82, sparse.cpp:247-259).
+ * read_obj: "v x y z" / "f i j k" (1-based) records; query sizes with
+ * positions = corners = NULL; errors carry the reference's messages
+ * (decmg_io_last_error). write_obj / write_matrix_market write level k's
+ * complex or its L, P, R ('L', 'P', 'R'; tags laplacian0 / prolongation /
+ * restriction) byte-for-byte as the reference's writers do. */
+DECMG_API const char* decmg_io_last_error(void);
+DECMG_API int decmg_read_obj(const char* path, double* positions, int* nv, int* corners, int* nt);
+DECMG_API int decmg_gpu_write_obj(decmg_gpu_ctx* ctx, int level, const char* path);
+DECMG_API int decmg_gpu_write_matrix_market(decmg_gpu_ctx* ctx, int level, char op, const char* path);
 /* kind: "uniform" (2u-1), "ylm" (Y_3^2 + 1e-3 N(0,1)), "sinsin", "lr" (L*u);
  * RHS j uses seed + j. Writes [n0][nrhs]. Dirichlet contexts zero boundary rows. */
 DECMG_API int decmg_gpu_make_rhs(decmg_gpu_ctx* ctx, const char* kind, uint64_t seed, int nrhs, double* b);

@@ -721,6 +721,7 @@ int64_t orc_get(const orc_hier* h, int k, const char* name, void* out) {
     if (!strcmp(name, "positions")) COPY_OUT(lv->m.pos, 3 * (int64_t)nv, double);
     if (!strcmp(name, "edges")) COPY_OUT(lv->m.edges, 2 * (int64_t)lv->m.ne, int);
     if (!strcmp(name, "triangles")) COPY_OUT(lv->m.tris, 3 * (int64_t)lv->m.nt, int);
+    if (!strcmp(name, "corners")) COPY_OUT(lv->m.corners, 3 * (int64_t)lv->m.nt, int);
     if (!strcmp(name, "dual_areas")) COPY_OUT(lv->area, nv, double);
     if (!strcmp(name, "boundary")) COPY_OUT(lv->bd, nv, int);
     if (!strcmp(name, "L_rp")) COPY_OUT(lv->L_rp, nv + 1, int);

@@ -487,6 +487,31 @@ int cmd_pcg(const Case& c, int k, const std::string& rhs, std::uint64_t seed, co
     return 0;
 }
 
+// I/O parity: write_obj / write_matrix_market of level `lvl` (mesh_io.cpp:71-82,
+// sparse.cpp:247-259) and read_obj (mesh_io.cpp:19-69) + its mesh hash.
+int cmd_write(const Case& c, int k, int lvl, const std::string& what, const std::string& out) {
+    const auto tower = tower_of(c, k);
+    MultigridHierarchy h = build_hierarchy(c.base, tower);
+    const auto& L = h.level(lvl);
+    if (what == "obj") write_obj(*L.mesh, out);
+    else if (what == "L") L.ops.laplacian.write_matrix_market(out);
+    else if (what == "P") L.prolongation.write_matrix_market(out);
+    else if (what == "R") L.restriction.write_matrix_market(out);
+    else throw std::invalid_argument("write: obj|L|P|R");
+    return 0;
+}
+
+int cmd_readobj(const std::string& path) {
+    try {
+        const auto m = read_obj(path);
+        std::printf("{\"nv\": %d, \"ne\": %d, \"nt\": %d, \"hash\": \"%llu\"}\n", m->num_vertices(),
+                    m->num_edges(), m->num_triangles(), (unsigned long long)m->hash());
+    } catch (const std::exception& e) {
+        std::printf("{\"error\": \"%s\"}\n", e.what());
+    }
+    return 0;
+}
+
 // per-cycle cost = (t(2n) - t(n)) / n with run_cycle from x0 = 0, plus a full
 // gmg_solve. nrhs independent right-hand sides are solved one after another
 // (the reference has no batched solve).
@@ -538,12 +563,15 @@ int cmd_time(const Case& c, int k, bool dirichlet, int nrhs, int ncyc, double to
 
 int main(int argc, char** argv) {
     try {
+        if (argc == 3 && std::string(argv[1]) == "readobj") return cmd_readobj(argv[2]);
         if (argc < 4) {
             std::fprintf(stderr,
                          "usage: ref_harness structure <case> <k> <bc> [full]\n"
                          "       ref_harness cycles <case> <k> <bc> <rhs> <seed> <ncycles> [jacobi|gs|sgs]\n"
                          "       ref_harness solve <case> <k> <bc> <rhs> <seed> <tol> <maxc> [jacobi|gs|sgs]\n"
                          "       ref_harness time <case> <k> <bc> <nrhs> <ncyc> <tol> <maxc> [jacobi|gs|sgs]\n"
+                         "       ref_harness write <case> <k> <level> <obj|L|P|R> <out>\n"
+                         "       ref_harness readobj <file.obj>\n"
                          "       ref_harness pcg <case> <k> neumann <rhs> <seed> <V|W> <pre> <post> <cycles> <tol> <maxit> [jacobi|gs|sgs]\n");
             return 2;
         }
@@ -552,6 +580,7 @@ int main(int argc, char** argv) {
         const int k = std::atoi(argv[3]);
         const bool dirichlet = argc > 4 && std::string(argv[4]) == "dirichlet";
         if (cmd == "structure") return cmd_structure(c, k, dirichlet, argc > 5 && std::string(argv[5]) == "full");
+        if (cmd == "write" && argc >= 7) return cmd_write(c, k, std::atoi(argv[4]), argv[5], argv[6]);
         if (cmd == "pcg" && argc >= 13)
             return cmd_pcg(c, k, argv[5], std::strtoull(argv[6], nullptr, 10), argv[7], std::atoi(argv[8]),
                            std::atoi(argv[9]), std::atoi(argv[10]), std::atof(argv[11]), std::atoi(argv[12]),

@@ -82,6 +82,10 @@ SIGNATURES = {
                                        C.POINTER(C.c_double)]),
     "decmg_gpu_launch_count": (C.c_int64, [C.c_void_p]),
     "decmg_base_mesh": (C.c_int, [C.c_char_p, C.c_void_p, C.POINTER(C.c_int), C.c_void_p, C.POINTER(C.c_int)]),
+    "decmg_io_last_error": (C.c_char_p, []),
+    "decmg_read_obj": (C.c_int, [C.c_char_p, C.c_void_p, C.POINTER(C.c_int), C.c_void_p, C.POINTER(C.c_int)]),
+    "decmg_gpu_write_obj": (C.c_int, [C.c_void_p, C.c_int, C.c_char_p]),
+    "decmg_gpu_write_matrix_market": (C.c_int, [C.c_void_p, C.c_int, C.c_char, C.c_char_p]),
     "decmg_gpu_make_rhs": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_int, C.c_void_p]),
     "decmg_gpu_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_int]),
     "decmg_gpu_dist_create": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_uint,

@@ -198,6 +198,20 @@ def base_mesh(spec: str):
     return pos, tri
 
 
+def read_obj(path) -> tuple:
+    """read_obj (mesh_io.cpp:19-69): (positions [nv,3], corner triples [nt,3]);
+    RuntimeError with the reference's message on a malformed file."""
+    lib = _lib.load()
+    nv, nt = C.c_int(), C.c_int()
+    p = str(path).encode()
+    if lib.decmg_read_obj(p, None, C.byref(nv), None, C.byref(nt)) != _lib.DECMG_OK:
+        raise RuntimeError(lib.decmg_io_last_error().decode())
+    pos = np.empty((nv.value, 3), dtype=np.float64)
+    tri = np.empty((nt.value, 3), dtype=np.int32)
+    check(lib.decmg_read_obj(p, _ptr(pos), C.byref(nv), _ptr(tri), C.byref(nt)))
+    return pos, tri
+
+
 class MultigridHierarchy:
     """Device-resident level hierarchy (finest level = 0)."""
 
@@ -322,6 +336,15 @@ class MultigridHierarchy:
         if self._lib.decmg_gpu_export(self._ctx, k, name.encode(), _ptr(out)) < 0:
             raise _lib.CudaError("export failed")
         return out
+
+    def write_obj(self, k: int, path) -> None:
+        """write_obj (mesh_io.cpp:71-82) of level k's complex."""
+        check(self._lib.decmg_gpu_write_obj(self._ctx, k, str(path).encode()), self._ctx)
+
+    def write_matrix_market(self, k: int, op: str, path) -> None:
+        """SparseOperator::write_matrix_market (sparse.cpp:247-259) of level k's
+        L, P or R ('L' / 'P' / 'R')."""
+        check(self._lib.decmg_gpu_write_matrix_market(self._ctx, k, op.encode(), str(path).encode()), self._ctx)
 
     def mesh_hash(self, k: int) -> int:
         h = C.c_uint64()

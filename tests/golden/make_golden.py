@@ -76,6 +76,46 @@ PCG = [
 ]
 
 
+# write_obj / write_matrix_market (mesh_io.cpp:71-82, sparse.cpp:247-259):
+# sha256 of the reference's output bytes; read_obj (mesh_io.cpp:19-69): a
+# reference-written OBJ fixture and the reference's verdicts on malformed files
+WRITES = [("ico", "3", "0", w) for w in ("obj", "L", "P", "R")] + [("ico", "3", "1", "L")] + \
+         [("square+cubic", "2", "0", w) for w in ("obj", "L", "P", "R")] + [("equi:4:8:1.0", "2", "1", "obj")]
+BAD_OBJ = {
+    "vertex": "v 0 0\nf 1 2 3\n",
+    "face_index": "v 0 0 0\nv 1 0 0\nv 0 1 0\nf 1 2 x\n",
+    "quad": "v 0 0 0\nv 1 0 0\nv 0 1 0\nv 1 1 0\nf 1 2 3 4\n",
+    "range": "v 0 0 0\nv 1 0 0\nf 1 2 3\n",
+    "record": "v 0 0 0\nvn 0 0 1\n",
+    "slash": "v 0 0 0\nv 1 0 0\nv 0 1 0\nf 1/1 2/2 3/3\n",
+    "empty": "# nothing\n\n",
+    "ok_comments": "# tri\nv 0 0 0\n\nv 1 0 0\nv 0 1 0\nf 1 2 3\n",
+}
+
+
+def make_io():
+    import hashlib
+    import tempfile
+    out = {"writes": [], "bad_obj": {}}
+    with tempfile.TemporaryDirectory() as td:
+        for case, k, lvl, what in WRITES:
+            f = Path(td) / "out"
+            subprocess.run([str(HARNESS), "write", case, k, lvl, what, str(f)], check=True)
+            out["writes"].append({"case": case, "k": int(k), "level": int(lvl), "what": what,
+                                  "sha256": hashlib.sha256(f.read_bytes()).hexdigest()})
+        for name, text in BAD_OBJ.items():
+            f = Path(td) / f"{name}.obj"
+            f.write_text(text)
+            verdict = run(["readobj", str(f)])
+            if "error" in verdict:  # paths differ between runs: keep the part after the file name
+                verdict["error"] = verdict["error"].replace(str(f), "<path>")
+            out["bad_obj"][name] = {"text": text, "verdict": verdict}
+        obj = OUT / "ico2_ref.obj"
+        subprocess.run([str(HARNESS), "write", "ico", "2", "0", "obj", str(obj)], check=True)
+        out["ico2_ref_obj"] = run(["readobj", str(obj)])
+    (OUT / "io.json").write_text(json.dumps(out, indent=1) + "\n")
+
+
 def run(argv):
     res = subprocess.run([str(HARNESS), *argv], check=True, capture_output=True, text=True)
     return json.loads(res.stdout)
@@ -85,6 +125,8 @@ def main() -> int:
     if not HARNESS.exists():
         subprocess.run(["make", "-C", str(ROOT / "oracle"), "ref", "-j8"], check=True)
     only = set(sys.argv[1:])  # optional: regenerate just these stems
+    if not only or "io" in only:
+        make_io()
     for stem, argv in STRUCTURE + CYCLES + SOLVES + PCG:
         if only and stem not in only:
             continue
