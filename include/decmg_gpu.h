@@ -101,10 +101,12 @@ DECMG_API const char* decmg_gpu_last_error(const decmg_gpu_ctx* ctx);
  * per-level sweep counts (NULL = pre_all/post_all on every level).
  * smoother (SmootherConfig, multigrid.hpp:55-60; smooth, multigrid.cpp:95-120):
  * weighted Jacobi, Gauss-Seidel (forward lexicographic, bit-identical to the
- * sequential sweep via a level schedule) or symmetric Gauss-Seidel (forward +
- * reverse per iteration); the reference's fixed-iteration CG smoother is not
- * offered. The partitioned solve (decmg_gpu_dist_*) runs Jacobi only. */
-enum { DECMG_SMOOTHER_JACOBI = 0, DECMG_SMOOTHER_GS = 1, DECMG_SMOOTHER_SGS = 2 };
+ * sequential sweep via a level schedule), symmetric Gauss-Seidel (forward +
+ * reverse per iteration) or the fixed-iteration CG smoother (cg_fixed,
+ * multigrid.cpp:63-91; deterministic tree dots, so within rounding of the
+ * reference's sequential ones). The partitioned solve (decmg_gpu_dist_*) runs
+ * Jacobi only. */
+enum { DECMG_SMOOTHER_JACOBI = 0, DECMG_SMOOTHER_GS = 1, DECMG_SMOOTHER_SGS = 2, DECMG_SMOOTHER_CG = 3 };
 typedef struct {
     const char* walk;
     const int* pre;

@@ -30,7 +30,7 @@ namespace decmg {
 enum class Smoother { GaussSeidel, SymmetricGaussSeidel, WeightedJacobi, Cg };
 
 struct SmootherConfig {
-    // device path: weighted Jacobi (default) or (symmetric) Gauss-Seidel; no Cg
+    // device path: weighted Jacobi (default), (symmetric) Gauss-Seidel, Cg
     Smoother method = Smoother::WeightedJacobi;
     double jacobi_omega = 2.0 / 3.0;
 };
@@ -100,14 +100,14 @@ struct PlanC {
     std::vector<int> pre, post;
     decmg_gpu_plan s{};
     explicit PlanC(const CyclePlan& p) : pre(p.pre), post(p.post) {
-        if (p.smoother.method == Smoother::Cg)
-            throw std::invalid_argument("smoother: the device implements weighted Jacobi and (symmetric) Gauss-Seidel");
+
         for (Transition t : p.walk) walk.push_back(t == Transition::Down ? 'd' : 'u');
         s.walk = walk.c_str();
         s.pre = pre.data();
         s.post = post.data();
         s.smoother = p.smoother.method == Smoother::GaussSeidel            ? DECMG_SMOOTHER_GS
                      : p.smoother.method == Smoother::SymmetricGaussSeidel ? DECMG_SMOOTHER_SGS
+                     : p.smoother.method == Smoother::Cg                   ? DECMG_SMOOTHER_CG
                                                                             : DECMG_SMOOTHER_JACOBI;
         s.jacobi_omega = p.smoother.jacobi_omega;
     }

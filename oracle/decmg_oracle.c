@@ -862,11 +862,47 @@ static int gs_sweep(const level_t* lv, double* x, const double* b, int reverse) 
 
 typedef struct { int pre, post, smoother; double omega; } plan_t;
 
+/* cg_fixed (proj/src/multigrid.cpp:63-91) with the level's dual areas as
+ * weights (cycle_once passes lvl.ops.dual_areas): sequential weighted dots,
+ * no convergence exit; breaks on rr == 0 or zero curvature. */
+static void cg_smooth(const level_t* lv, double* x, const double* b, int iters) {
+    const int n = lv->m.nv;
+    const double* w = lv->area;
+    double* r = NEW(double, n);
+    double* p = NEW(double, n);
+    double* Ap = NEW(double, n);
+    csr_apply(n, lv->L_rp, lv->L_ci, lv->L_v, x, r);
+    for (int i = 0; i < n; ++i) r[i] = b[i] - r[i];
+    memcpy(p, r, (size_t)n * sizeof(double));
+    double rr = 0.0;
+    for (int i = 0; i < n; ++i) rr += w[i] * r[i] * r[i];
+    for (int it = 0; it < iters; ++it) {
+        if (rr == 0.0) break;
+        csr_apply(n, lv->L_rp, lv->L_ci, lv->L_v, p, Ap);
+        double curv = 0.0;
+        for (int i = 0; i < n; ++i) curv += w[i] * p[i] * Ap[i];
+        if (curv == 0.0) break;
+        const double alpha = rr / curv;
+        for (int i = 0; i < n; ++i) x[i] += alpha * p[i];
+        for (int i = 0; i < n; ++i) r[i] -= alpha * Ap[i];
+        double rn = 0.0;
+        for (int i = 0; i < n; ++i) rn += w[i] * r[i] * r[i];
+        const double beta = rn / rr;
+        for (int i = 0; i < n; ++i) p[i] = r[i] + beta * p[i];
+        rr = rn;
+    }
+    free(r); free(p); free(Ap);
+}
+
 /* smooth (proj/src/multigrid.cpp:95-120): 0 weighted Jacobi, 1 Gauss-Seidel,
- * 2 symmetric Gauss-Seidel (forward then reverse per iteration) */
+ * 2 symmetric Gauss-Seidel (forward then reverse per iteration), 3 cg_fixed */
 static int smooth(const level_t* lv, double* x, const double* b, const plan_t* p, int iters, double* s) {
     for (int it = 0; it < iters; ++it) {
         int rc;
+        if (p->smoother == 3) {  /* Smoother::Cg: one call runs `iters` CG steps */
+            cg_smooth(lv, x, b, iters);
+            return 0;
+        }
         if (p->smoother == 0) {
             rc = jacobi_sweep(lv, x, b, p->omega, s);
         } else {

@@ -396,6 +396,7 @@ SmootherConfig jacobi() { return SmootherConfig{Smoother::WeightedJacobi, 2.0 / 
 SmootherConfig smoother_of(const std::string& name) {
     if (name == "gs") return SmootherConfig{Smoother::GaussSeidel, 2.0 / 3.0};
     if (name == "sgs") return SmootherConfig{Smoother::SymmetricGaussSeidel, 2.0 / 3.0};
+    if (name == "cg") return SmootherConfig{Smoother::Cg, 2.0 / 3.0};
     return jacobi();
 }
 
@@ -567,12 +568,12 @@ int main(int argc, char** argv) {
         if (argc < 4) {
             std::fprintf(stderr,
                          "usage: ref_harness structure <case> <k> <bc> [full]\n"
-                         "       ref_harness cycles <case> <k> <bc> <rhs> <seed> <ncycles> [jacobi|gs|sgs]\n"
-                         "       ref_harness solve <case> <k> <bc> <rhs> <seed> <tol> <maxc> [jacobi|gs|sgs]\n"
-                         "       ref_harness time <case> <k> <bc> <nrhs> <ncyc> <tol> <maxc> [jacobi|gs|sgs]\n"
+                         "       ref_harness cycles <case> <k> <bc> <rhs> <seed> <ncycles> [jacobi|gs|sgs|cg]\n"
+                         "       ref_harness solve <case> <k> <bc> <rhs> <seed> <tol> <maxc> [jacobi|gs|sgs|cg]\n"
+                         "       ref_harness time <case> <k> <bc> <nrhs> <ncyc> <tol> <maxc> [jacobi|gs|sgs|cg]\n"
                          "       ref_harness write <case> <k> <level> <obj|L|P|R> <out>\n"
                          "       ref_harness readobj <file.obj>\n"
-                         "       ref_harness pcg <case> <k> neumann <rhs> <seed> <V|W> <pre> <post> <cycles> <tol> <maxit> [jacobi|gs|sgs]\n");
+                         "       ref_harness pcg <case> <k> neumann <rhs> <seed> <V|W> <pre> <post> <cycles> <tol> <maxit> [jacobi|gs|sgs|cg]\n");
             return 2;
         }
         const std::string cmd = argv[1];

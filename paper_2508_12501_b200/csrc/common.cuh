@@ -175,6 +175,8 @@ struct decmg_gpu_ctx {
     double* io_x = nullptr;
     double* pcg_buf = nullptr;  // GMG-PCG vectors (pcg.cu), 5 x [n0][max_nrhs], allocated on first use
     double* pcg_s = nullptr;    // GMG-PCG per-lane scalars [8][32]
+    double* cgs_buf = nullptr;  // CG smoother vectors r, p, Ap: 3 x [n0][max_nrhs], on first use
+    double* cgs_s = nullptr;    // CG smoother per-lane scalars [6][32] + done flags
     cudaStream_t io_stream = nullptr;        // chunked host copies (stage_rhs)
     std::vector<cudaEvent_t> io_events;
     int64_t launch_count = 0;

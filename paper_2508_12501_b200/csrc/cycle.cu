@@ -34,9 +34,8 @@ Status make_plan(const decmg_gpu_ctx* c, const decmg_gpu_plan* p, Plan* out) {
     const int L = static_cast<int>(c->lv.size());
     Plan q;
     if (p && p->smoother != DECMG_SMOOTHER_JACOBI && p->smoother != DECMG_SMOOTHER_GS &&
-        p->smoother != DECMG_SMOOTHER_SGS)
-        return Status::Err(DECMG_INVALID_ARGUMENT,
-                           "smoother: the device implements weighted Jacobi and (symmetric) Gauss-Seidel");
+        p->smoother != DECMG_SMOOTHER_SGS && p->smoother != DECMG_SMOOTHER_CG)
+        return Status::Err(DECMG_INVALID_ARGUMENT, "smoother: unknown smoother");
     q.smoother = p ? p->smoother : DECMG_SMOOTHER_JACOBI;
     q.omega = p ? p->jacobi_omega : 2.0 / 3.0;
     if (p && p->walk) {

@@ -176,9 +176,87 @@ struct Driver {
         return Status::Ok();
     }
 
+    // cg_fixed (multigrid.cpp:63-91) on level k with the level's dual areas as
+    // weights (smooth's `weights`, cycle_once passes lvl.ops.dual_areas):
+    // iters CG steps from the current x, per lane, no convergence exit. The
+    // weighted dots are fixed-shape trees (the reference's are sequential).
+    Status cg_smooth(int k, int iters) {
+        DG_TRY(ensure_x(k));
+        Level& L = c->lv[k];
+        const int n = L.nv;
+        const size_t nv0 = static_cast<size_t>(c->lv[0].nv) * c->max_nrhs;
+        if (!c->cgs_buf) {
+            DG_TRY(dalloc(c, &c->cgs_buf, 3 * nv0));
+            DG_TRY(dalloc(c, &c->cgs_s, 8 * 32));
+        }
+        double* r = c->cgs_buf;
+        double* p = r + nv0;
+        double* ap = p + nv0;
+        double* rr = c->cgs_s;
+        double* curv = c->cgs_s + 32;
+        double* alpha = c->cgs_s + 64;
+        double* rrn = c->cgs_s + 96;
+        double* beta = c->cgs_s + 128;
+        int* done = reinterpret_cast<int*>(c->cgs_s + 160);
+        double* x = xcur(L);
+        const double* b = bptr(k);
+        const double* w = L.area_i;
+        const int cls = k == 0 ? kFineSweep : kCoarseLevels;
+        const unsigned g = rows_grid(n);
+        const double mbytes = 12.0 * L.nnzL + 4.0 * (n + 1) + 16.0 * n * nrhs;
+        auto spmv = [&](const double* v, const double* bb, double* y, int op) -> Status {
+            if (L.Le_ci && tpr <= 8) {
+                if (op == OP_RES_STORE)
+                    return pipe_w<OP_RES_STORE>(L.Le_w, cls, mbytes, n, L.Le_ci, L.Le_v, L.Le_row, v, bb, y, nullptr,
+                                                nullptr, 0.0, nullptr);
+                return pipe_w<OP_SPMV>(L.Le_w, cls, mbytes, n, L.Le_ci, L.Le_v, L.Le_row, v, nullptr, y, nullptr,
+                                       nullptr, 0.0, nullptr);
+            }
+            return launch(c, cls, mbytes, [&] {
+                if (op == OP_RES_STORE) {
+                    DISPATCH_BP(key, (k_residual<BP, RPT, 0, true><<<g, kBlock, 0, c->stream>>>(
+                                        n, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v, nullptr, v, bb, y, nullptr)))
+                } else {
+                    DISPATCH_BP(key, (k_spmv<BP, RPT, 0><<<g, kBlock, 0, c->stream>>>(n, nrhs, L.Lo_rp, L.Lo_ci, L.Lo_v,
+                                                                                      nullptr, v, y, nullptr)))
+                }
+            });
+        };
+        auto wdot = [&](const double* a, const double* bb, double* out) -> Status {
+            DG_TRY(launch(c, cls, 24.0 * n * nrhs, [&] {
+                DISPATCH_BP(key, k_wdot<BP, RPT><<<g, kBlock, 0, c->stream>>>(n, nrhs, w, a, bb, c->red));
+            }));
+            return reduce_partials(partial_blocks(n), out, 0, nullptr);
+        };
+        const size_t vb = sizeof(double) * static_cast<size_t>(n) * nrhs;
+        DG_TRY(spmv(x, b, r, OP_RES_STORE));  // r = b - A x
+        DG_CUDA(cudaMemcpyAsync(p, r, vb, cudaMemcpyDeviceToDevice, c->stream));
+        DG_CUDA(cudaMemsetAsync(done, 0, sizeof(int) * 32, c->stream));
+        DG_TRY(wdot(r, r, rr));
+        for (int it = 0; it < iters; ++it) {
+            DG_TRY(launch(c, kNorms, 0.0, [&] { k_cgs_start<<<1, 32, 0, c->stream>>>(nrhs, rr, done); }));
+            DG_TRY(spmv(p, nullptr, ap, OP_SPMV));
+            DG_TRY(wdot(p, ap, curv));
+            DG_TRY(launch(c, kNorms, 0.0, [&] { k_cgs_alpha<<<1, 32, 0, c->stream>>>(nrhs, rr, curv, alpha, done); }));
+            DG_TRY(launch(c, cls, 48.0 * n * nrhs, [&] {
+                DISPATCH_BP(key, (k_cgs_update<BP, RPT, false><<<g, kBlock, 0, c->stream>>>(n, nrhs, alpha, done, x, r,
+                                                                                          p, ap)));
+            }));
+            DG_TRY(wdot(r, r, rrn));
+            DG_TRY(launch(c, kNorms, 0.0, [&] { k_cgs_beta<<<1, 32, 0, c->stream>>>(nrhs, rr, rrn, beta, done); }));
+            DG_TRY(launch(c, cls, 24.0 * n * nrhs, [&] {
+                DISPATCH_BP(key, (k_cgs_update<BP, RPT, true><<<g, kBlock, 0, c->stream>>>(n, nrhs, beta, done, nullptr,
+                                                                                         r, p, nullptr)));
+            }));
+        }
+        L.x_zero = false;
+        return Status::Ok();
+    }
+
     Status smooth(int k, int iters, const Plan& plan) {
         Level& L = c->lv[k];
         if (iters <= 0) return Status::Ok();
+        if (plan.smoother == DECMG_SMOOTHER_CG) return cg_smooth(k, iters);
         if (plan.smoother != DECMG_SMOOTHER_JACOBI) {  // smooth (multigrid.cpp:95-120)
             if (L.zero_diag_row >= 0)
                 return Status::Err(DECMG_RUNTIME,

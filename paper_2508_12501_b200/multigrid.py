@@ -40,8 +40,8 @@ class SmootherConfig:
     # sweep. The device implements weighted Jacobi (multigrid.cpp:36-56) and
     # the forward / symmetric Gauss-Seidel sweeps (multigrid.cpp:13-34) as a
     # level schedule that is bit-identical to the sequential sweep (DESIGN.md
-    # "Gauss-Seidel"); the default stays Jacobi (BASELINE north star). Cg is
-    # not offered on the device.
+    # "Gauss-Seidel"); the default stays Jacobi (BASELINE north star). Cg =
+    # cg_fixed (multigrid.cpp:63-91) with tree dots (within rounding).
     method: Smoother = Smoother.WeightedJacobi
     jacobi_omega: float = 2.0 / 3.0
 
@@ -171,12 +171,13 @@ def _ptr(a: np.ndarray):
     return a.ctypes.data_as(C.c_void_p)
 
 
-_SMOOTHER_C = {Smoother.WeightedJacobi: 0, Smoother.GaussSeidel: 1, Smoother.SymmetricGaussSeidel: 2}
+_SMOOTHER_C = {Smoother.WeightedJacobi: 0, Smoother.GaussSeidel: 1, Smoother.SymmetricGaussSeidel: 2,
+               Smoother.Cg: 3}
 
 
 def _plan_struct(plan: CyclePlan, levels: int):
     if plan.smoother.method not in _SMOOTHER_C:
-        raise ValueError("smoother: the device implements weighted Jacobi and (symmetric) Gauss-Seidel")
+        raise ValueError("smoother: unknown smoother")
     plan.validate(levels)
     pre = (C.c_int * levels)(*plan.pre[:levels])
     post = (C.c_int * levels)(*plan.post[:levels])

@@ -53,6 +53,8 @@ CYCLES = [
     ("cycles_square_cubic_3_dirichlet_sinsin", ["cycles", "square+cubic", "3", "dirichlet", "sinsin", "0", "8"]),
     ("cycles_ico_cubic_3_uniform", ["cycles", "ico+cubic", "3", "neumann", "uniform", "1", "8"]),
     ("cycles_ico_cubic_2_ylm_gs", ["cycles", "ico+cubic", "2", "neumann", "ylm", "2", "5", "gs"]),
+    ("cycles_ico_4_uniform_cg", ["cycles", "ico", "4", "neumann", "uniform", "1", "6", "cg"]),
+    ("cycles_square_4_dirichlet_sinsin_cg", ["cycles", "square", "4", "dirichlet", "sinsin", "0", "5", "cg"]),
 ]
 SOLVES = [
     # BASELINE configs 1-3 (config 3 takes ~30 s of reference setup)
@@ -65,6 +67,7 @@ SOLVES = [
     ("solve_config1_sgs", ["solve", "square", "4", "dirichlet", "sinsin", "0", "1e-8", "200", "sgs"]),
     ("solve_ico_cubic_3_ylm", ["solve", "ico+cubic", "3", "neumann", "ylm", "1", "1e-8", "300"]),
     ("solve_square_cubic_4_uniform", ["solve", "square+cubic", "4", "neumann", "uniform", "5", "1e-8", "300"]),
+    ("solve_config2_cg", ["solve", "ico", "6", "neumann", "ylm", "1", "1e-8", "200", "cg"]),
 ]
 PCG = [
     # gmg_preconditioned_cg (solvers.cpp:118-130): <rhs> <seed> <V|W> <pre> <post> <cycles> <tol> <maxit> [smoother]

