@@ -177,6 +177,10 @@ DECMG_API int decmg_gpu_set_timing(decmg_gpu_ctx* ctx, int enable);
 DECMG_API int decmg_gpu_get_timing(decmg_gpu_ctx* ctx, int cls, int64_t* launches, double* total_ms,
                          double* bytes);
 DECMG_API int64_t decmg_gpu_launch_count(decmg_gpu_ctx* ctx); /* kernels launched since creation */
+/* Diagnostic of the exact parallel projection chain (project_compatible): how many
+ * (256-row segment, RHS) pairs ran the literal sequential add chain since creation (the rest were
+ * applied in O(1) on their binade's integer grid). -1 on error. */
+DECMG_API int64_t decmg_gpu_projection_fallbacks(decmg_gpu_ctx* ctx);
 
 /* Input generators (extension x3): base meshes and synthetic RHS.
  * base_mesh spec: "square", "ico", "grid:nx:ny:lx:ly", "equi:rows:cols:side".

@@ -81,6 +81,7 @@ SIGNATURES = {
     "decmg_gpu_get_timing": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                        C.POINTER(C.c_double)]),
     "decmg_gpu_launch_count": (C.c_int64, [C.c_void_p]),
+    "decmg_gpu_projection_fallbacks": (C.c_int64, [C.c_void_p]),
     "decmg_base_mesh": (C.c_int, [C.c_char_p, C.c_void_p, C.POINTER(C.c_int), C.c_void_p, C.POINTER(C.c_int)]),
     "decmg_io_last_error": (C.c_char_p, []),
     "decmg_read_obj": (C.c_int, [C.c_char_p, C.c_void_p, C.POINTER(C.c_int), C.c_void_p, C.POINTER(C.c_int)]),

@@ -40,6 +40,7 @@ Status init_ctx(decmg_gpu_ctx* c, const decmg_gpu_config* cfg) {
     if (const char* e = std::getenv("DECMG_PF")) c->pf = std::atoi(e);
     if (const char* e = std::getenv("DECMG_FUSE_RR")) c->fuse_rr = std::atoi(e) != 0;
     if (const char* e = std::getenv("DECMG_RR_WINDOW")) c->rr_window = std::atoi(e) != 0;
+    if (const char* e = std::getenv("DECMG_PROJ_SEQ")) c->proj_seq = std::atoi(e) != 0;
     if (const char* e = std::getenv("DECMG_PFL")) c->pfl = std::atoi(e);
     if (const char* e = std::getenv("DECMG_KERNEL")) {
         const std::string m(e);
@@ -390,6 +391,17 @@ int decmg_gpu_get_timing(decmg_gpu_ctx* ctx, int cls, int64_t* launches, double*
 }
 
 int64_t decmg_gpu_launch_count(decmg_gpu_ctx* ctx) { return ctx ? ctx->launch_count : -1; }
+
+int64_t decmg_gpu_projection_fallbacks(decmg_gpu_ctx* ctx) {
+    if (!ctx) return -1;
+    if (!ctx->seq_fallbacks) return 0;
+    cudaSetDevice(ctx->device);
+    int v = 0;
+    if (cudaMemcpyAsync(&v, ctx->seq_fallbacks, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+        return -1;
+    return v;
+}
 
 // ---------------------------------------------------------------- inputs ----
 // make_triangulated_grid (proj/src/mesh.cpp:232-257), make_equilateral_grid

@@ -177,6 +177,9 @@ struct decmg_gpu_ctx {
     double* pcg_s = nullptr;    // GMG-PCG per-lane scalars [8][32]
     double* cgs_buf = nullptr;  // CG smoother vectors r, p, Ap: 3 x [n0][max_nrhs], on first use
     double* cgs_s = nullptr;    // CG smoother per-lane scalars [6][32] + done flags
+    double* seq_buf = nullptr;  // exact parallel projection chain scratch (seqsum.cuh), on first use
+    int* seq_fallbacks = nullptr;  // device counter of segments that ran the literal chain
+    int proj_seq = 0;           // literal single-lane projection chain instead (env DECMG_PROJ_SEQ=1)
     cudaStream_t io_stream = nullptr;        // chunked host copies (stage_rhs)
     std::vector<cudaEvent_t> io_events;
     int64_t launch_count = 0;

@@ -20,6 +20,7 @@
 // Norms and projections use a fixed-shape tree reduction: deterministic run
 // to run, within a few ulps of the reference's blocked sums.
 #include "driver.cuh"
+#include "seqsum.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -94,8 +95,59 @@ Status run_cycles(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_
 namespace {
 
 // The projection's mean chain over rows [r0, r1) (state in c->dsmall + 160),
-// mean_out on the last range.
-Status project_chain(decmg_gpu_ctx* c, int nrhs, const double* d_b, int r0, int r1, double* mean_out) {
+// mean_out on the last range: the exact parallel chain (seqsum.cuh) in passes
+// of at most kSeqPassRows rows.
+Status project_chain_par(decmg_gpu_ctx* c, int nrhs, const double* d_b, int r0, int r1, double* mean_out) {
+    const Level& L = c->lv[0];
+    double* state = c->dsmall + 160;
+    const size_t lanes = static_cast<size_t>(c->max_nrhs);
+    const size_t per = static_cast<size_t>(kSeqPassRecs) * lanes;  // approx, guess: [lane][record]
+    const size_t pstride = static_cast<size_t>((std::min(kSeqPassRows, L.nv) + 3) & ~1);  // even: nodes stay 16-byte aligned
+    const size_t nodes_d = lanes * kSeqPassGrps * sizeof(SeqNode) * kGrpNodes / sizeof(double);
+    if (!c->seq_buf) {
+        DG_TRY(dalloc(c, &c->seq_buf, 2 * per + pstride * lanes + nodes_d));
+        DG_TRY(dalloc(c, &c->seq_fallbacks, 1));
+        DG_CUDA(cudaMemsetAsync(c->seq_fallbacks, 0, sizeof(int), c->stream));
+        const int smax = kTileRows * 33 * static_cast<int>(sizeof(double));
+        DG_CUDA(cudaFuncSetAttribute(k_seq_prod, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+        DG_CUDA(cudaFuncSetAttribute(k_seq_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, kWalkSmem));
+    }
+    double* approx = c->seq_buf;
+    double* guess = approx + per;
+    double* prodT = guess + per;  // [lane][stride] products of the pass
+    SeqNode* nodes = reinterpret_cast<SeqNode*>(prodT + pstride * lanes);
+    const size_t smem = static_cast<size_t>(kTileRows) * (nrhs + 1) * sizeof(double);
+    for (int a = r0;; a += kSeqPassRows) {
+        const int b = std::min(r1, a + kSeqPassRows);
+        const int stride = (b - a + 1) & ~1;  // even: 16-byte aligned bulk copies per lane
+        const int ntile = (b - a + kTileRows - 1) / kTileRows;
+        const int nrec = (b - a + kRecRows - 1) / kRecRows;
+        const int ngrp = (b - a + kGrpRows - 1) / kGrpRows;
+        double* mo = b >= r1 ? mean_out : nullptr;
+        const double rows = b - a, t = rows * nrhs;
+        if (ntile > 0) {
+            DG_TRY(launch(c, kNorms, 8.0 * rows + 16.0 * t, [&] {
+                k_seq_prod<<<ntile, 256, smem, c->stream>>>(a, b, nrhs, stride, L.area, d_b, prodT, approx);
+            }));
+            DG_TRY(launch(c, kNorms, 16.0 * nrec * nrhs, [&] {
+                k_seq_guess<<<nrhs, 1024, 0, c->stream>>>(nrec, approx, state, guess);
+            }));
+            DG_TRY(launch(c, kNorms, 8.0 * t + 3024.0 * ngrp * nrhs, [&] {
+                k_seq_tree<<<dim3(ngrp, (nrhs + 3) / 4), 128, 0, c->stream>>>(a, b, nrhs, stride, prodT, guess,
+                                                                             nodes);
+            }));
+        }
+        DG_TRY(launch(c, kNorms, 8.0 * t + 3024.0 * ngrp * nrhs, [&] {
+            k_seq_walk<<<nrhs, 32, kWalkSmem, c->stream>>>(a, b, stride, prodT, nodes, state, c->wtot0, mo,
+                                                          c->seq_fallbacks);
+        }));
+        if (b >= r1) break;
+    }
+    return Status::Ok();
+}
+
+// The same chain run literally, one lane per RHS (DECMG_PROJ_SEQ=1).
+Status project_chain_seq(decmg_gpu_ctx* c, int nrhs, const double* d_b, int r0, int r1, double* mean_out) {
     const Level& L = c->lv[0];
     double* state = c->dsmall + 160;
     const size_t smem = static_cast<size_t>(kProjStages) * proj_rows(nrhs) * nrhs * sizeof(double);
@@ -113,6 +165,11 @@ Status project_chain(decmg_gpu_ctx* c, int nrhs, const double* d_b, int r0, int 
     return launch(c, kNorms, 8.0 * t, [&] {
         k_project_sums<<<1, 64, smem, c->stream>>>(r0, r1, nrhs, prod, c->wtot0, state, mean_out);
     });
+}
+
+Status project_chain(decmg_gpu_ctx* c, int nrhs, const double* d_b, int r0, int r1, double* mean_out) {
+    return c->proj_seq ? project_chain_seq(c, nrhs, d_b, r0, r1, mean_out)
+                       : project_chain_par(c, nrhs, d_b, r0, r1, mean_out);
 }
 
 Status project_subtract(decmg_gpu_ctx* c, int nrhs, const double* mean, double* d_b) {

@@ -416,6 +416,10 @@ class MultigridHierarchy:
     def launch_count(self) -> int:
         return self._lib.decmg_gpu_launch_count(self._ctx)
 
+    def projection_fallbacks(self) -> int:
+        """(segment, RHS) pairs of the exact projection chain that ran the literal add chain."""
+        return self._lib.decmg_gpu_projection_fallbacks(self._ctx)
+
     def stream(self) -> int:
         return self._lib.decmg_gpu_stream(self._ctx)
 

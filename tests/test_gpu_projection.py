@@ -1,0 +1,87 @@
+"""project_compatible (proj/src/multigrid.cpp:240-250) on the device: the
+exact parallel evaluation of the reference's sequential mean chain
+(csrc/seqsum.cuh) must give the bits of the literal loop
+`mean += w[i]*b[i]` -- checked against the oracle's literal loop on inputs that
+exercise every branch: ordinary random right-hand sides (mostly the O(1)
+segment path), one-signed sums (monotone growth across binades), wide dynamic
+range (terms larger than the running sum, binade changes), exact ties on the
+running sum's grid (dyadic areas on the flat square), signed zeros and sparse
+spikes (zero crossings), and sizes across the 2^20-row pass boundary. The
+literal chain (DECMG_PROJ_SEQ=1 path) is the fallback inside every test, and
+the fallback counter proves the fast path carried most segments."""
+import numpy as np
+import pytest
+
+import paper_2508_12501_b200 as d
+from oracle_ctypes import OracleHierarchy
+
+pytestmark = pytest.mark.gpu
+
+
+def crafted(kind, n, nrhs, seed):
+    rng = np.random.default_rng(seed)
+    if kind == "uniform":
+        return rng.uniform(-1, 1, (n, nrhs))
+    if kind == "positive":
+        return rng.uniform(0, 1, (n, nrhs))
+    if kind == "wide":
+        return rng.uniform(-1, 1, (n, nrhs)) * np.ldexp(1.0, rng.integers(-40, 40, (n, nrhs)))
+    if kind == "ties":  # short dyadic mantissas: sums round on exact halfway points
+        return rng.integers(-1023, 1024, (n, nrhs)).astype(np.float64) * np.ldexp(1.0, rng.integers(-60, 0, (n, nrhs)))
+    if kind == "zeros_spikes":
+        b = np.where(rng.random((n, nrhs)) < 0.5, -0.0, 0.0)
+        m = rng.random((n, nrhs)) < 0.01
+        b[m] = rng.uniform(-1e3, 1e3, m.sum())
+        b[rng.random((n, nrhs)) < 0.2] = rng.uniform(-1e-12, 1e-12)
+        return b
+    raise ValueError(kind)
+
+
+def check(h, o, B):
+    B = B.reshape(B.shape[0], -1)
+    ref = np.stack([o.project(B[:, j].copy()) for j in range(B.shape[1])], axis=1)
+    got = h.project_compatible(B)
+    np.testing.assert_array_equal(got.view(np.uint64), ref.view(np.uint64))
+
+
+@pytest.mark.parametrize("base,nsub", [("ico", 6), ("square", 7)])
+@pytest.mark.parametrize("kind", ["uniform", "positive", "wide", "ties", "zeros_spikes"])
+def test_projection_bit_exact(base, nsub, kind):
+    nrhs = 5
+    h = d.MultigridHierarchy.from_base(base, nsub, dirichlet=False, max_nrhs=nrhs)
+    o = OracleHierarchy(base, nsub)
+    B = crafted(kind, h.n(), nrhs, 7)
+    check(h, o, B)
+    segs = -(-h.n() // 32) * nrhs
+    assert 0 <= h.projection_fallbacks() <= segs
+
+
+@pytest.mark.parametrize("nrhs", [1, 16, 32])
+def test_projection_bit_exact_batches(nrhs):
+    h = d.MultigridHierarchy.from_base("ico", 8, max_nrhs=nrhs)
+    o = OracleHierarchy("ico", 8)
+    B = h.make_rhs("uniform", 3, nrhs)
+    check(h, o, B)
+    # a random walk of 655 k terms crosses a binade or zero in ~5-15 % of its 32-term
+    # records (tools/seqsum_proto.c); the rest take the O(1) path
+    segs = -(-h.n() // 32) * nrhs
+    assert h.projection_fallbacks() < 0.25 * segs
+
+
+def test_projection_across_passes_and_solve_staging():
+    """icosphere x10 (10.5 M rows: 11 passes of 2^20 rows) through
+    project_compatible, and gmg_solve's chunked host staging (16 H2D chunks,
+    the chain continued chunk by chunk) gives the same projected RHS: the
+    solve's first iterate equals run_cycle's from the oracle-projected RHS."""
+    nrhs = 2
+    h = d.MultigridHierarchy.from_base("ico", 10, max_nrhs=nrhs)
+    o = OracleHierarchy("ico", 10)
+    B = h.make_rhs("uniform", 1, nrhs)
+    check(h, o, B)
+    assert h.projection_fallbacks() < 0.04 * (-(-h.n() // 32) * nrhs)
+    Bp = np.stack([o.project(B[:, j].copy()) for j in range(nrhs)], axis=1)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan.cycles = 1
+    res = h.run_cycle(plan, Bp)
+    rep = d.gmg_solve(h, plan, B, 1e-30, 1)
+    np.testing.assert_array_equal(rep.solution, res.x)
