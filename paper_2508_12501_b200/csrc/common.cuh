@@ -115,6 +115,13 @@ struct Level {
     int* S2_halo = nullptr;  // ELL row indices of halo rows
     int* S2_slot = nullptr;  // [npad * Le_w]
     int S2_maxhalo = -1;     // -1: no tiles
+    // Wavefront sweep pairs (pair.cu): per 56-row ELL tile its neighbour tiles,
+    // sweep-1 completion counters (epoch-based, never reset) and a completed-tile count.
+    int* pr_deps = nullptr;
+    unsigned* pr_flags = nullptr;
+    unsigned long long* pr_done = nullptr;
+    unsigned pr_epoch = 0;
+    int pr_rows = 0;
     // Exact lexicographic Gauss-Seidel as a level schedule (setup.cu
     // build_gs_schedule): phase p of the forward (f) / reverse (r) sweep is
     // the internal rows gs?_rows[gs?_ptr[p] .. gs?_ptr[p+1]), ascending.
@@ -180,6 +187,9 @@ struct decmg_gpu_ctx {
     double* seq_buf = nullptr;  // exact parallel projection chain scratch (seqsum.cuh), on first use
     int* seq_fallbacks = nullptr;  // device counter of segments that ran the literal chain
     int proj_seq = 0;           // literal single-lane projection chain instead (env DECMG_PROJ_SEQ=1)
+    int pair = 0;               // wavefront sweep pairs (pair.cu), opt-in: env DECMG_PAIR=1 (slower)
+    int pair_ch = 1;            // tiles per chunk (env DECMG_PAIR_CH)
+    int pair_lag = 1;           // sweep-2 lag in steps (env DECMG_PAIR_LAG)
     cudaStream_t io_stream = nullptr;        // chunked host copies (stage_rhs)
     std::vector<cudaEvent_t> io_events;
     int64_t launch_count = 0;
@@ -227,6 +237,10 @@ Status launch(decmg_gpu_ctx* c, int cls, double bytes, F&& f) {
 inline unsigned grid_for(int64_t threads, int block) {
     return static_cast<unsigned>((threads + block - 1) / block);
 }
+
+// pair.cu: two Jacobi sweeps in one wavefront pass (x -> x'' in place, x' in x[cur ^ 1])
+Status pair_sweeps(decmg_gpu_ctx* c, int k, int key, int nrhs, double omega, const double* b, double* partial,
+                   int* grid, double bytes, int cls);
 
 // setup.cu
 Status build_from_base(decmg_gpu_ctx* c, const double* pos, int nv, const int* corners, int nt,

@@ -272,6 +272,19 @@ struct Driver {
         const double R = nrhs;
         for (int it = 0; it < iters;) {
             const bool fuse_norm = k == 0 && it == 0 && fuse_hist && !L.x_zero;
+            if (iters - it >= 2 && c->pair && !L.x_zero && L.Le_ci && tpr <= 8 && !(fuse_norm && fuse_hook)) {
+                // two sweeps in one wavefront pass (pair.cu); x'' lands in x[cur]
+                const double bytes = 2.0 * (12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R);
+                int g = 0;
+                DG_TRY(pair_sweeps(c, k, key, nrhs, plan.omega, bptr(k), fuse_norm ? c->red : nullptr, &g, bytes,
+                                   k == 0 ? kFineSweep : kCoarseLevels));
+                if (fuse_norm) {
+                    DG_TRY(reduce_partials(g, fuse_hist, 2, fuse_denom));
+                    fuse_hist = nullptr;
+                }
+                it += 2;
+                continue;
+            }
             if (iters - it >= 2 && L.S2_maxhalo >= 0 && tpr <= 8 && c->sweep2) {
                 DG_TRY(sweep_pair(k, plan, fuse_norm ? fuse_hist : nullptr));
                 it += 2;

@@ -85,3 +85,22 @@ def test_projection_across_passes_and_solve_staging():
     res = h.run_cycle(plan, Bp)
     rep = d.gmg_solve(h, plan, B, 1e-30, 1)
     np.testing.assert_array_equal(rep.solution, res.x)
+
+
+@pytest.mark.parametrize("nsub,nrhs", [(6, 16), (6, 5), (7, 1)])
+def test_wavefront_sweep_pairs_bitwise(monkeypatch, nsub, nrhs):
+    """The opt-in wavefront sweep pairs (csrc/pair.cu, DECMG_PAIR=1) give the
+    iterates of separate sweeps bit for bit (V(2,2): every post-smoothing pair
+    and the level-0 pre-smoothing pair with its fused residual norm)."""
+    plan_cycles = 3
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("DECMG_PAIR", flag)
+        h = d.MultigridHierarchy.from_base("ico", nsub, max_nrhs=nrhs)
+        B = h.project_compatible(h.make_rhs("uniform", 4, nrhs))
+        plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+        plan.cycles = plan_cycles
+        res = h.run_cycle(plan, B)
+        out[flag] = (res.x, np.asarray(res.residual_history))
+    np.testing.assert_array_equal(out["1"][0], out["0"][0])
+    np.testing.assert_allclose(out["1"][1], out["0"][1], rtol=1e-13, atol=0)
