@@ -283,19 +283,40 @@ def run_ours(args, world, rank, local):
                                        C.c_void_p(hx.data_ptr()), hhist.ctypes.data_as(C.c_void_p),
                                        done.ctypes.data_as(C.c_void_p), fin.ctypes.data_as(C.c_void_p)), h.ctx)
     solve_once()  # warm
-    e2e_steps = max(1, min(args.steps, 3))
+    # single-call latency: one gmg_solve, host to host
     barrier(world)
     t0 = time.perf_counter()
-    cyc_units = 0.0
-    for _ in range(e2e_steps):
-        solve_once()
-        cyc_units += float(n) * float(done.sum())
+    solve_once()
+    latency_s = max_over_ranks(world, time.perf_counter() - t0)
+    single_done = done.tolist()
+    # e2e throughput: a stream of K independent 16-RHS solves through the public
+    # batch API (decmg_gpu_solve_batches): each step's H2D and D2H are inside
+    # the timed region and overlap the neighbouring steps' cycles
+    e2e_steps = max(3, min(args.steps, 8))
+    bptrs = (C.c_void_p * e2e_steps)(*([hb.data_ptr()] * e2e_steps))
+    xptrs = (C.c_void_p * e2e_steps)(*([hx.data_ptr()] * e2e_steps))
+    bhist = np.zeros((e2e_steps, 200, args.nrhs))
+    bdone = np.zeros((e2e_steps, args.nrhs), dtype=np.int32)
+    bfin = np.zeros((e2e_steps, args.nrhs))
+    def solve_stream(k):
+        _lib.check(lib.decmg_gpu_solve_batches(h.ctx, C.byref(ps), args.nrhs, k, bptrs, 1e-8, 200, xptrs,
+                                               bhist.ctypes.data_as(C.c_void_p), bdone.ctypes.data_as(C.c_void_p),
+                                               bfin.ctypes.data_as(C.c_void_p)), h.ctx)
+    solve_stream(2)  # warm (allocates the second buffers and streams)
+    barrier(world)
+    t0 = time.perf_counter()
+    solve_stream(e2e_steps)
     e2e_s = max_over_ranks(world, time.perf_counter() - t0)
-    cyc_units = sum_over_ranks(world, cyc_units)
+    cyc_units = sum_over_ranks(world, float(n) * float(bdone.sum()))
+    assert bdone.tolist() == [single_done] * e2e_steps, "batched solves must match the single solve"
     e2e = {"value": cyc_units / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(B.nbytes),
-           "d2h_bytes_per_step": int(B.nbytes + hhist[:1].nbytes), "step": "gmg_solve(tol=1e-8) of the 16-RHS batch "
-           "from pinned host memory to pinned host memory", "time_to_1e-8_s": e2e_s / e2e_steps,
-           "cycles_to_1e-8": done.tolist(), "final_rel_residual_max": float(fin.max())}
+           "d2h_bytes_per_step": int(B.nbytes), "steps": e2e_steps,
+           "step": "one gmg_solve(tol=1e-8) of the 16-RHS batch from pinned host memory to pinned host memory; "
+                   "K steps through decmg_gpu_solve_batches (step k+1's upload + projection and step k-1's "
+                   "download overlap step k's cycles)",
+           "ms_per_step": 1e3 * e2e_s / e2e_steps, "time_to_1e-8_s": latency_s,
+           "single_call_value": float(n) * float(sum(single_done)) / latency_s,
+           "cycles_to_1e-8": single_done, "final_rel_residual_max": float(bfin.max())}
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",

@@ -131,6 +131,17 @@ DECMG_API int decmg_gpu_solve(decmg_gpu_ctx* ctx, const decmg_gpu_plan* plan, in
                     const double* x0, double tol, int max_cycles, double* x_out, double* hist_out,
                     int* cycles_done, double* final_out);
 
+/* A stream of nbatch independent gmg_solve calls (extension x6: no reference
+ * counterpart; a caller would otherwise loop over decmg_gpu_solve). Batch k =
+ * host arrays b[k] -> x_out[k] ([n][nrhs] each, pinned memory for overlap),
+ * every batch bit-identical to its own decmg_gpu_solve; batch k+1's upload and
+ * projection and batch k-1's download run on copy/auxiliary streams while
+ * batch k cycles. hist_out [nbatch][max_cycles][nrhs], cycles_done and
+ * final_out [nbatch][nrhs] (each may be NULL). x0 = 0. */
+DECMG_API int decmg_gpu_solve_batches(decmg_gpu_ctx* ctx, const decmg_gpu_plan* plan, int nrhs, int nbatch,
+                                      const double* const* b, double tol, int max_cycles, double* const* x_out,
+                                      double* hist_out, int* cycles_done, double* final_out);
+
 /* gmg_preconditioned_cg (proj/src/solvers.cpp:118-130): weighted CG
  * (solvers.cpp:56-116, dual-area weights) preconditioned by inner_cycles
  * cycles of the inner plan from zero; projects b (Neumann hierarchies only).

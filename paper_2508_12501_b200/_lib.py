@@ -66,6 +66,8 @@ SIGNATURES = {
                                        C.c_int, C.c_void_p, C.c_void_p]),
     "decmg_gpu_solve": (C.c_int, [C.c_void_p, C.POINTER(decmg_gpu_plan), C.c_int, C.c_void_p, C.c_void_p,
                                   C.c_double, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "decmg_gpu_solve_batches": (C.c_int, [C.c_void_p, C.POINTER(decmg_gpu_plan), C.c_int, C.c_int, C.c_void_p, C.c_double, C.c_int,
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "decmg_gpu_pcg": (C.c_int, [C.c_void_p, C.POINTER(decmg_gpu_plan), C.c_int, C.c_int, C.c_void_p, C.c_double,
                                 C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "decmg_gpu_run_cycles_dev": (C.c_int, [C.c_void_p, C.POINTER(decmg_gpu_plan), C.c_int, C.c_void_p,

@@ -34,7 +34,11 @@ Status init_ctx(decmg_gpu_ctx* c, const decmg_gpu_config* cfg) {
     DG_CUDA(cudaGetDeviceCount(&ndev));
     if (c->device < 0 || c->device >= ndev) return Status::Err(DECMG_INVALID_ARGUMENT, "no such CUDA device");
     DG_CUDA(cudaSetDevice(c->device));
-    DG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    // the context stream runs the V-cycle at the highest priority: staging work
+    // of a batch stream (solve_batches, lowest priority) fills in around it
+    int prio_lo = 0, prio_hi = 0;
+    DG_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    DG_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi));
     DG_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
     if (const char* e = std::getenv("DECMG_SWEEP2")) c->sweep2 = std::atoi(e) != 0;
     if (const char* e = std::getenv("DECMG_PF")) c->pf = std::atoi(e);
@@ -69,6 +73,12 @@ void destroy_ctx(decmg_gpu_ctx* c) {
     if (c->hsmall) cudaFreeHost(c->hsmall);
     if (c->hist_dev) cudaFree(c->hist_dev);
     for (cudaEvent_t e : c->io_events) cudaEventDestroy(e);
+    for (cudaStream_t s : {c->io_stream, c->aux_stream, c->d2h_stream})
+        if (s) cudaStreamSynchronize(s);
+    for (cudaEvent_t e : {c->ev_stage[0], c->ev_stage[1], c->ev_d2h[0], c->ev_d2h[1], c->ev_start})
+        if (e) cudaEventDestroy(e);
+    if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+    if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
     if (c->io_stream) cudaStreamDestroy(c->io_stream);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -227,6 +237,19 @@ int decmg_gpu_solve(decmg_gpu_ctx* ctx, const decmg_gpu_plan* plan, int nrhs, co
     if (x_out)
         API_TRY(ctx, cuda_status(cudaMemcpyAsync(x_out, ctx->io_x, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H x"));
     API_TRY(ctx, cuda_status(cudaStreamSynchronize(ctx->stream), "gmg_solve"));
+    return DECMG_OK;
+}
+
+int decmg_gpu_solve_batches(decmg_gpu_ctx* ctx, const decmg_gpu_plan* plan, int nrhs, int nbatch,
+                            const double* const* b, double tol, int max_cycles, double* const* x_out,
+                            double* hist_out, int* cycles_done, double* final_out) {
+    if (!ctx) return DECMG_INVALID_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    Plan p;
+    API_TRY(ctx, make_plan(ctx, plan, &p));
+    if (nrhs < 1 || nrhs > ctx->max_nrhs)
+        return fail(ctx, Status::Err(DECMG_INVALID_ARGUMENT, "nrhs must be in [1, max_nrhs]"));
+    API_TRY(ctx, solve_batches(ctx, p, nrhs, nbatch, b, tol, max_cycles, x_out, hist_out, cycles_done, final_out));
     return DECMG_OK;
 }
 

@@ -172,6 +172,7 @@ struct decmg_gpu_ctx {
     size_t red_cap = 0;         // doubles
     double* dsmall = nullptr;   // per-RHS device scalars (256 doubles)
     double* hsmall = nullptr;   // pinned host mirror
+    double* hsmall_dev = nullptr;  // its device alias (mapped pinned memory)
     double* coarse_scratch = nullptr;
     double* bproj = nullptr;    // projected RHS for solve [n0][max_nrhs]
     double* xsol = nullptr;     // solve snapshot [n0][max_nrhs]
@@ -191,6 +192,14 @@ struct decmg_gpu_ctx {
     int pair_ch = 1;            // tiles per chunk (env DECMG_PAIR_CH)
     int pair_lag = 1;           // sweep-2 lag in steps (env DECMG_PAIR_LAG)
     cudaStream_t io_stream = nullptr;        // chunked host copies (stage_rhs)
+    // solve_batches (cycle.cu): second input/output buffers, staging and copy-out streams
+    double* bproj2 = nullptr;
+    double* io_x2 = nullptr;
+    cudaStream_t aux_stream = nullptr;
+    cudaStream_t d2h_stream = nullptr;
+    cudaEvent_t ev_stage[2] = {nullptr, nullptr};
+    cudaEvent_t ev_d2h[2] = {nullptr, nullptr};
+    cudaEvent_t ev_start = nullptr;
     std::vector<cudaEvent_t> io_events;
     int64_t launch_count = 0;
     int rpt = 4;                // right-hand sides per thread in the vector mapping (env DECMG_RPT)
@@ -265,8 +274,10 @@ Status run_cycles(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_
                   const double* d_x0, int ncycles, double* d_x, double* d_hist);
 Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, const double* d_x0,
              double tol, int max_cycles, double* d_x, double* h_hist, int* cycles_done,
-             double* h_final, bool staged = false);
-Status stage_rhs(decmg_gpu_ctx* c, int nrhs, const double* h_b, bool project);
+             double* h_final, bool staged = false, const double* bsrc = nullptr);
+Status stage_rhs(decmg_gpu_ctx* c, int nrhs, const double* h_b, bool project, double* dst = nullptr);
+Status solve_batches(decmg_gpu_ctx* c, const Plan& plan, int nrhs, int nbatch, const double* const* h_b, double tol,
+                     int max_cycles, double* const* h_x, double* h_hist, int* cycles_done, double* h_final);
 // pcg.cu: gmg_preconditioned_cg (proj/src/solvers.cpp:118-130)
 Status pcg(decmg_gpu_ctx* c, const Plan& inner, int inner_cycles, int nrhs, const double* d_b, double tol,
            int maxiter, double* d_x, double* h_hist, int* iters, int* converged, double* h_final);

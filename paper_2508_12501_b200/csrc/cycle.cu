@@ -23,6 +23,9 @@
 #include "seqsum.cuh"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <functional>
 
@@ -197,10 +200,10 @@ Status project_compatible(decmg_gpu_ctx* c, int nrhs, double* d_b) {
 // Host right-hand side -> c->bproj, projected (Neumann): the H2D copy runs in
 // chunks on a second stream and the sequential mean chain follows chunk by
 // chunk on the context stream, so the copy hides under the chain.
-Status stage_rhs(decmg_gpu_ctx* c, int nrhs, const double* h_b, bool project) {
+Status stage_rhs(decmg_gpu_ctx* c, int nrhs, const double* h_b, bool project, double* dst) {
     DG_TRY(check_nrhs(c, nrhs));
     const int n = c->lv[0].nv;
-    double* dst = c->bproj;
+    if (!dst) dst = c->bproj;
     if (!project) {
         DG_CUDA(cudaMemcpyAsync(dst, h_b, sizeof(double) * n * nrhs, cudaMemcpyHostToDevice, c->stream));
         return Status::Ok();
@@ -228,27 +231,45 @@ Status stage_rhs(decmg_gpu_ctx* c, int nrhs, const double* h_b, bool project) {
         }
         DG_CUDA(cudaEventRecord(c->io_events[k], c->io_stream));
         DG_CUDA(cudaStreamWaitEvent(c->stream, c->io_events[k], 0));
-        if (r1 > r0 || k == kChunks - 1) DG_TRY(project_chain(c, nrhs, dst, r0, r1, k == kChunks - 1 ? mean : nullptr));
+        static const bool skip_chain = std::getenv("DECMG_DEBUG_NOCHAIN") != nullptr;  // timing experiment only
+        if (!skip_chain && (r1 > r0 || k == kChunks - 1))
+            DG_TRY(project_chain(c, nrhs, dst, r0, r1, k == kChunks - 1 ? mean : nullptr));
     }
     return project_subtract(c, nrhs, mean, dst);
+}
+
+// A few device scalars -> c->hsmall, written by a kernel through the mapped
+// pinned buffer rather than a copy engine (a 16-double copy would queue behind
+// a concurrent 1.3 GB download in solve_batches), then synchronise.
+Status small_to_host(decmg_gpu_ctx* c, const double* d_src, int n) {
+    if (!c->hsmall_dev) {
+        void* p = nullptr;
+        DG_CUDA(cudaHostGetDevicePointer(&p, c->hsmall, 0));
+        c->hsmall_dev = static_cast<double*>(p);
+    }
+    DG_TRY(launch(c, kNorms, 16.0 * n, [&] { k_small_copy<<<1, 32, 0, c->stream>>>(n, d_src, c->hsmall_dev); }));
+    DG_CUDA(cudaStreamSynchronize(c->stream));
+    return Status::Ok();
 }
 
 // gmg_solve (proj/src/solvers.cpp:251-279), batched: each RHS stops at its
 // own cycle count; its solution is the iterate of that cycle.
 Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, const double* d_x0,
              double tol, int max_cycles, double* d_x, double* h_hist, int* cycles_done,
-             double* h_final, bool staged) {
+             double* h_final, bool staged, const double* bsrc) {
     DG_TRY(check_nrhs(c, nrhs));
     if (max_cycles < 0) return Status::Err(DECMG_INVALID_ARGUMENT, "gmg_solve: max_cycles >= 0");
     Level& L0 = c->lv[0];
-    if (!staged) {  // staged: stage_rhs already left the projected RHS in c->bproj
+    if (!bsrc) bsrc = c->bproj;
+    if (!staged) {  // staged: stage_rhs already left the projected RHS in bsrc
         const size_t nbytes = sizeof(double) * L0.nv * nrhs;
         DG_CUDA(cudaMemcpyAsync(c->bproj, d_b, nbytes, cudaMemcpyDeviceToDevice, c->stream));
         if (!c->dirichlet) DG_TRY(project_compatible(c, nrhs, c->bproj));  // in the reference numbering
+        bsrc = c->bproj;
     }
-    Driver dr{c, nrhs, bp_of(nrhs), L0.ord ? L0.b : c->bproj};
+    Driver dr{c, nrhs, bp_of(nrhs), L0.ord ? L0.b : bsrc};
     dr.init();
-    if (L0.ord) DG_TRY(dr.to_internal(c->bproj, L0.b));
+    if (L0.ord) DG_TRY(dr.to_internal(bsrc, L0.b));
     double* denom = c->dsmall;
     double* dres = c->dsmall + 256;
     DG_TRY(dr.load_x0(d_x0));
@@ -261,15 +282,13 @@ Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, co
     int cyc = 0;
     if (max_cycles == 0) {
         DG_TRY(dr.resnorm(dres, denom));
-        DG_CUDA(cudaMemcpyAsync(c->hsmall, dres, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, c->stream));
-        DG_CUDA(cudaStreamSynchronize(c->stream));
+        DG_TRY(small_to_host(c, dres, nrhs));
         for (int l = 0; l < nrhs; ++l) final_res[l] = c->hsmall[l];
     }
     // Record the residual of the iterate after `cyc` cycles (in dres) and
     // retire the right-hand sides that reached tol; xsrc holds that iterate.
     auto check = [&](const double* xsrc) -> Status {
-        DG_CUDA(cudaMemcpyAsync(c->hsmall, dres, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, c->stream));
-        DG_CUDA(cudaStreamSynchronize(c->stream));
+        DG_TRY(small_to_host(c, dres, nrhs));
         unsigned fin = 0;
         for (int l = 0; l < nrhs; ++l) {
             if (!(active & (1u << l))) continue;
@@ -330,6 +349,76 @@ Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, co
         if (cycles_done) cycles_done[l] = done[l];
         if (h_final) h_final[l] = final_res[l];
     }
+    return Status::Ok();
+}
+
+// A stream of independent gmg_solve batches (extension x6):
+// batch k+1's host-to-device copy and projection chain run on their own
+// streams while batch k cycles, and batch k's solution goes back to the host
+// while batch k+1 cycles. Each batch is exactly one gmg_solve (same kernels,
+// same bits); only the copies and the projection overlap other batches' work.
+Status solve_batches(decmg_gpu_ctx* c, const Plan& plan, int nrhs, int nbatch, const double* const* h_b, double tol,
+                     int max_cycles, double* const* h_x, double* h_hist, int* cycles_done, double* h_final) {
+    DG_TRY(check_nrhs(c, nrhs));
+    if (nbatch < 0) return Status::Err(DECMG_INVALID_ARGUMENT, "gmg_solve_batches: nbatch >= 0");
+    if (max_cycles < 0) return Status::Err(DECMG_INVALID_ARGUMENT, "gmg_solve: max_cycles >= 0");
+    const int n0 = c->lv[0].nv;
+    const size_t n = static_cast<size_t>(n0) * nrhs;
+    for (int k = 0; k < nbatch; ++k)
+        if (!h_b || !h_b[k]) return Status::Err(DECMG_INVALID_ARGUMENT, "gmg_solve_batches: rhs is null");
+    if (!c->bproj2) {
+        DG_TRY(dalloc(c, &c->bproj2, static_cast<size_t>(n0) * c->max_nrhs));
+        DG_TRY(dalloc(c, &c->io_x2, static_cast<size_t>(n0) * c->max_nrhs));
+        int prio_lo = 0, prio_hi = 0;
+        DG_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        DG_CUDA(cudaStreamCreateWithPriority(&c->aux_stream, cudaStreamNonBlocking, prio_lo));
+        DG_CUDA(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            DG_CUDA(cudaEventCreateWithFlags(&c->ev_stage[i], cudaEventDisableTiming));
+            DG_CUDA(cudaEventCreateWithFlags(&c->ev_d2h[i], cudaEventDisableTiming));
+        }
+        DG_CUDA(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+    }
+    double* bp[2] = {c->bproj, c->bproj2};
+    double* xo[2] = {c->io_x, c->io_x2};
+    const bool project = !c->dirichlet;
+    // staging of batch k on the auxiliary stream (its kernels are launched on
+    // c->stream, so the context stream is swapped for the duration)
+    auto stage = [&](int k) -> Status {
+        if (c->proj_seq) {  // the literal chain uses the residual scratch: no overlap
+            DG_TRY(stage_rhs(c, nrhs, h_b[k], project, bp[k & 1]));
+            return cuda_status(cudaEventRecord(c->ev_stage[k & 1], c->stream), "stage event");
+        }
+        cudaStream_t keep = c->stream;
+        c->stream = c->aux_stream;
+        Status s = stage_rhs(c, nrhs, h_b[k], project, bp[k & 1]);
+        if (s.ok()) s = cuda_status(cudaEventRecord(c->ev_stage[k & 1], c->aux_stream), "stage event");
+        c->stream = keep;
+        return s;
+    };
+    DG_CUDA(cudaEventRecord(c->ev_start, c->stream));  // after everything already queued on the context
+    DG_CUDA(cudaStreamWaitEvent(c->aux_stream, c->ev_start, 0));
+    DG_CUDA(cudaStreamWaitEvent(c->d2h_stream, c->ev_start, 0));
+    if (nbatch > 0) DG_TRY(stage(0));
+    for (int k = 0; k < nbatch; ++k) {
+        if (k + 1 < nbatch) DG_TRY(stage(k + 1));  // overlaps batch k's cycles
+        DG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_stage[k & 1], 0));
+        if (k >= 2) DG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_d2h[k & 1], 0));  // xo[k & 1] copied out
+        const size_t ho = static_cast<size_t>(k) * (max_cycles > 0 ? max_cycles : 1) * nrhs;
+        const auto t_solve = std::chrono::steady_clock::now();
+        DG_TRY(solve(c, plan, nrhs, nullptr, nullptr, tol, max_cycles, xo[k & 1], h_hist ? h_hist + ho : nullptr,
+                     cycles_done ? cycles_done + static_cast<size_t>(k) * nrhs : nullptr,
+                     h_final ? h_final + static_cast<size_t>(k) * nrhs : nullptr, true, bp[k & 1]));
+        // solve returned after synchronising the context stream: xo[k & 1] holds batch k
+        if (std::getenv("DECMG_DEBUG"))
+            std::fprintf(stderr, "solve_batches: batch %d solve %.2f ms\n", k,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_solve).count());
+        if (h_x && h_x[k])
+            DG_CUDA(cudaMemcpyAsync(h_x[k], xo[k & 1], n * sizeof(double), cudaMemcpyDeviceToHost, c->d2h_stream));
+        DG_CUDA(cudaEventRecord(c->ev_d2h[k & 1], c->d2h_stream));
+    }
+    DG_CUDA(cudaStreamSynchronize(c->d2h_stream));
+    DG_CUDA(cudaStreamSynchronize(c->aux_stream));
     return Status::Ok();
 }
 

@@ -329,7 +329,7 @@ __device__ __forceinline__ bool node_apply(double& s, const SeqNode& n) {
 // single record whose fast path fails is chained literally (__dadd_rn in row
 // order); after a success it climbs back to the largest aligned node, so only
 // the records where the sum crosses a binade (or zero) run element by element.
-constexpr int kWalkStages = 4;
+constexpr int kWalkStages = 2;
 constexpr int kWalkNodeBytes = static_cast<int>(sizeof(SeqNode)) * kGrpNodes;  // 3024
 constexpr int kWalkStageBytes = kWalkNodeBytes + 16 + kGrpRows * 8;           // nodes | pad | products
 constexpr int kWalkSmem = kWalkStages * kWalkStageBytes;

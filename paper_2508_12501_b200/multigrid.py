@@ -455,6 +455,47 @@ def gmg_solve(h: MultigridHierarchy, plan: CyclePlan, b: np.ndarray, tol: float,
                        final_relative_residual=final.tolist(), wall_seconds=wall)
 
 
+def gmg_solve_batches(h: MultigridHierarchy, plan: CyclePlan, batches, tol: float, max_cycles: int,
+                      out=None) -> list:
+    """A stream of independent gmg_solve batches (extension x6, decmg_gpu_solve_batches):
+    batch k+1's upload and projection and batch k-1's download overlap batch
+    k's cycles; every batch equals its own gmg_solve bit for bit. batches: list
+    of [n] or [n, nrhs] arrays of one shape (pinned, e.g. torch pin_memory
+    views, for the copies to overlap); out: optional list of result arrays."""
+    nb = len(batches)
+    n = h.n()
+    arrs = [h._vec(b, n)[0] for b in batches]
+    nrhs = 1 if arrs and arrs[0].ndim == 1 else (arrs[0].shape[1] if arrs else 1)
+    if any(a.shape != arrs[0].shape for a in arrs):
+        raise ValueError("gmg_solve_batches: batches differ in shape")
+    outs = out if out is not None else [np.empty_like(a) for a in arrs]
+    ps, keep = _plan_struct(plan, h.levels())
+    bptrs = (C.c_void_p * max(nb, 1))(*[a.ctypes.data for a in arrs])
+    xptrs = (C.c_void_p * max(nb, 1))(*[o.ctypes.data for o in outs])
+    mc = max(max_cycles, 1)
+    hist = np.zeros((max(nb, 1), mc, nrhs))
+    done = np.zeros((max(nb, 1), nrhs), dtype=np.int32)
+    final = np.zeros((max(nb, 1), nrhs))
+    t0 = time.perf_counter()
+    check(h._lib.decmg_gpu_solve_batches(h.ctx, C.byref(ps), nrhs, nb, bptrs, tol, max_cycles, xptrs, _ptr(hist),
+                                         _ptr(done), _ptr(final)), h.ctx)
+    wall = time.perf_counter() - t0
+    reps = []
+    for k in range(nb):
+        if arrs[k].ndim == 1:
+            it = int(done[k, 0])
+            reps.append(SolveReport(solution=outs[k], residual_history=hist[k, :it, 0].tolist(), cumulative_seconds=[],
+                                    iterations=it, converged=bool(final[k, 0] <= tol),
+                                    final_relative_residual=float(final[k, 0]), wall_seconds=wall))
+        else:
+            reps.append(SolveReport(solution=outs[k], residual_history=[hist[k, : done[k, j], j].tolist()
+                                                                        for j in range(nrhs)],
+                                    cumulative_seconds=[], iterations=done[k].tolist(),
+                                    converged=(final[k] <= tol).tolist(), final_relative_residual=final[k].tolist(),
+                                    wall_seconds=wall))
+    return reps
+
+
 def gmg_preconditioned_cg(h: MultigridHierarchy, inner_plan: CyclePlan, b: np.ndarray, tol: float,
                           maxiter: int) -> SolveReport:
     """gmg_preconditioned_cg (solvers.cpp:118-130): weighted CG on the fine

@@ -104,3 +104,19 @@ def test_wavefront_sweep_pairs_bitwise(monkeypatch, nsub, nrhs):
         out[flag] = (res.x, np.asarray(res.residual_history))
     np.testing.assert_array_equal(out["1"][0], out["0"][0])
     np.testing.assert_allclose(out["1"][1], out["0"][1], rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("base,nsub,dirichlet,nrhs", [("ico", 7, False, 4), ("square", 6, True, 1)])
+def test_solve_batches_equal_single_solves(base, nsub, dirichlet, nrhs):
+    """decmg_gpu_solve_batches: each batch of the pipelined stream gives the
+    bits of its own gmg_solve (solution, history, cycle counts)."""
+    h = d.MultigridHierarchy.from_base(base, nsub, dirichlet=dirichlet, max_nrhs=nrhs)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    kinds = ["uniform", "lr", "uniform"] if not dirichlet else ["uniform", "sinsin", "lr"]
+    batches = [h.make_rhs(k, 10 + i, nrhs) if nrhs > 1 else h.make_rhs(k, 10 + i) for i, k in enumerate(kinds)]
+    reps = d.gmg_solve_batches(h, plan, batches, 1e-8, 60)
+    for b, rep in zip(batches, reps):
+        one = d.gmg_solve(h, plan, b, 1e-8, 60)
+        np.testing.assert_array_equal(rep.solution, one.solution)
+        assert rep.iterations == one.iterations
+        assert rep.residual_history == one.residual_history
