@@ -231,9 +231,7 @@ Status stage_rhs(decmg_gpu_ctx* c, int nrhs, const double* h_b, bool project, do
         }
         DG_CUDA(cudaEventRecord(c->io_events[k], c->io_stream));
         DG_CUDA(cudaStreamWaitEvent(c->stream, c->io_events[k], 0));
-        static const bool skip_chain = std::getenv("DECMG_DEBUG_NOCHAIN") != nullptr;  // timing experiment only
-        if (!skip_chain && (r1 > r0 || k == kChunks - 1))
-            DG_TRY(project_chain(c, nrhs, dst, r0, r1, k == kChunks - 1 ? mean : nullptr));
+        if (r1 > r0 || k == kChunks - 1) DG_TRY(project_chain(c, nrhs, dst, r0, r1, k == kChunks - 1 ? mean : nullptr));
     }
     return project_subtract(c, nrhs, mean, dst);
 }
