@@ -222,6 +222,46 @@ inline SolveReport gmg_solve(const MultigridHierarchy& h, const CyclePlan& plan,
     return rep;
 }
 
+// A stream of independent single-RHS gmg_solve calls (extension x6,
+// decmg_gpu_solve_batches): the next right-hand side's upload and projection
+// and the previous solution's download overlap the current solve's cycles.
+// Each report equals gmg_solve(h, plan, bs[k], tol, max_cycles) bit for bit.
+// (Host vectors are pageable here; pinned buffers through the C ABI overlap fully.)
+inline std::vector<SolveReport> gmg_solve_batches(const MultigridHierarchy& h, const CyclePlan& plan,
+                                                  const std::vector<std::vector<double>>& bs, double tol,
+                                                  int max_cycles) {
+    const auto t0 = std::chrono::steady_clock::now();
+    plan.validate(h.levels());
+    const int nb = static_cast<int>(bs.size());
+    for (const auto& b : bs)
+        if (static_cast<int>(b.size()) != h.fine_rows()) throw std::invalid_argument("run_cycle: rhs size mismatch");
+    detail::PlanC pc(plan);
+    std::vector<SolveReport> reps(bs.size());
+    std::vector<const double*> bp(bs.size());
+    std::vector<double*> xp(bs.size());
+    for (int k = 0; k < nb; ++k) {
+        reps[k].solution.resize(bs[k].size());
+        bp[k] = bs[k].data();
+        xp[k] = reps[k].solution.data();
+    }
+    const int mc = max_cycles > 0 ? max_cycles : 1;
+    std::vector<double> hist(static_cast<size_t>(nb) * mc), fin(nb);
+    std::vector<int> done(nb);
+    detail::check(decmg_gpu_solve_batches(h.handle(), &pc.s, 1, nb, bp.data(), tol, max_cycles, xp.data(),
+                                          hist.data(), done.data(), fin.data()),
+                  h.handle());
+    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (int k = 0; k < nb; ++k) {
+        reps[k].residual_history.assign(hist.begin() + static_cast<size_t>(k) * mc,
+                                        hist.begin() + static_cast<size_t>(k) * mc + done[k]);
+        reps[k].iterations = done[k];
+        reps[k].converged = fin[k] <= tol;
+        reps[k].final_relative_residual = fin[k];
+        reps[k].wall_seconds = wall;
+    }
+    return reps;
+}
+
 // gmg_preconditioned_cg (proj/src/solvers.cpp:118-130); inner_plan.cycles
 // cycles of the inner plan precondition each CG step. Single RHS, like the
 // reference; the C ABI (decmg_gpu_pcg) also takes [n][nrhs] batches.

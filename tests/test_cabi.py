@@ -53,8 +53,10 @@ int main() {
     // the GPU entry points must at least compile and link (no device here)
     auto solve = &decmg::gmg_solve;
     auto pcg = &decmg::gmg_preconditioned_cg;
+    auto batches = &decmg::gmg_solve_batches;
     (void)solve;
     (void)pcg;
+    (void)batches;
     return p.walk.size() == 6 && gs.smoother.method == decmg::Smoother::GaussSeidel ? 0 : 1;
 }
 """
