@@ -46,6 +46,7 @@ Status init_ctx(decmg_gpu_ctx* c, const decmg_gpu_config* cfg) {
     if (const char* e = std::getenv("DECMG_RR_WINDOW")) c->rr_window = std::atoi(e) != 0;
     if (const char* e = std::getenv("DECMG_PROJ_SEQ")) c->proj_seq = std::atoi(e) != 0;
     if (const char* e = std::getenv("DECMG_PAIR")) c->pair = std::atoi(e) != 0;
+    if (const char* e = std::getenv("DECMG_GRAPH")) c->graph = std::atoi(e) != 0;
     if (const char* e = std::getenv("DECMG_PAIR_CH")) c->pair_ch = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("DECMG_PAIR_LAG")) c->pair_lag = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("DECMG_PFL")) c->pfl = std::atoi(e);
@@ -77,6 +78,11 @@ void destroy_ctx(decmg_gpu_ctx* c) {
         if (s) cudaStreamSynchronize(s);
     for (cudaEvent_t e : {c->ev_stage[0], c->ev_stage[1], c->ev_d2h[0], c->ev_d2h[1], c->ev_start})
         if (e) cudaEventDestroy(e);
+    for (auto& e : c->graphs) {
+        cudaGraphExecDestroy(e.exec);
+        cudaGraphDestroy(e.graph);
+    }
+    if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
     if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
     if (c->io_stream) cudaStreamDestroy(c->io_stream);

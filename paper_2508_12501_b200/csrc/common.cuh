@@ -200,6 +200,16 @@ struct decmg_gpu_ctx {
     cudaEvent_t ev_stage[2] = {nullptr, nullptr};
     cudaEvent_t ev_d2h[2] = {nullptr, nullptr};
     cudaEvent_t ev_start = nullptr;
+    // device-side gmg_solve loops (cycle.cu solve_graph): instantiated graphs by key
+    struct GraphEntry {
+        std::string key;
+        cudaGraph_t graph;
+        cudaGraphExec_t exec;
+    };
+    std::vector<GraphEntry> graphs;
+    int graph = 1;              // env DECMG_GRAPH=0: host-driven cycle loop
+    cudaStream_t cap_stream = nullptr;
+    double* gstate_raw = nullptr;  // SolveState (rowkernels.cuh) of the device loop
     std::vector<cudaEvent_t> io_events;
     int64_t launch_count = 0;
     int rpt = 4;                // right-hand sides per thread in the vector mapping (env DECMG_RPT)

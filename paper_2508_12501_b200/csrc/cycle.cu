@@ -236,6 +236,114 @@ Status stage_rhs(decmg_gpu_ctx* c, int nrhs, const double* h_b, bool project, do
     return project_subtract(c, nrhs, mean, dst);
 }
 
+// Device-side gmg_solve loop: one CUDA graph per (plan, batch width, buffer
+// state) holding a WHILE node whose body is one cycle with the convergence
+// check in the middle -- [first level-0 sweep with the fused residual norm of
+// the current iterate, k_solve_check, copy of finished lanes] then an IF node
+// [rest of the cycle]. The host launches it once instead of synchronising on
+// every cycle's residual; every kernel and argument is the host loop's, so the
+// iterates and histories are the same bits. The body is captured from
+// Driver::one_cycle itself: the fused-norm hook adds the check kernels and
+// the IF node to the capture and redirects the rest of the cycle into the IF
+// body. Cycles preserve each level's ping-pong parity, so one captured cycle
+// is valid for every iteration; the key includes that parity.
+Status solve_graph(decmg_gpu_ctx* c, Driver& dr, const Plan& plan, int nrhs, unsigned all, double tol,
+                   int max_cycles, double* denom, double* dres, int64_t total) {
+    if (!c->gstate_raw) DG_TRY(dalloc(c, &c->gstate_raw, (sizeof(SolveState) + 7) / 8));
+    SolveState* gst = reinterpret_cast<SolveState*>(c->gstate_raw);
+    if (max_cycles > c->hist_cap) {
+        if (c->hist_dev) cudaFree(c->hist_dev);
+        c->hist_dev = nullptr;
+        c->hist_cap = 0;
+        DG_CUDA(cudaMalloc(&c->hist_dev, sizeof(double) * max_cycles * 32));
+        c->hist_cap = max_cycles;
+    }
+    std::string key = plan.walk + "|" + std::to_string(plan.smoother) + "|" + std::to_string(plan.omega) + "|" +
+                      std::to_string(nrhs) + "|" + std::to_string(reinterpret_cast<uintptr_t>(dr.b0)) + "|" +
+                      std::to_string(reinterpret_cast<uintptr_t>(c->hist_dev)) + "|" +
+                      std::to_string(reinterpret_cast<uintptr_t>(c->red)) + "|" + std::to_string(c->pair) + "|";
+    for (size_t k = 0; k < c->lv.size(); ++k)
+        key += std::to_string(plan.pre[k]) + "," + std::to_string(plan.post[k]) + "," +
+               std::to_string(c->lv[k].cur) + std::to_string(c->lv[k].x_zero ? 1 : 0) + ";";
+    cudaGraphExec_t exec = nullptr;
+    for (auto& e : c->graphs)
+        if (e.key == key) exec = e.exec;
+    if (!exec) {
+        cudaGraph_t g = nullptr;
+        DG_CUDA(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle hw;
+        DG_CUDA(cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams wp = {};
+        wp.type = cudaGraphNodeTypeConditional;
+        wp.conditional.handle = hw;
+        wp.conditional.type = cudaGraphCondTypeWhile;
+        wp.conditional.size = 1;
+        cudaGraphNode_t wn;
+        DG_CUDA(cudaGraphAddNode(&wn, g, nullptr, 0, &wp));
+        cudaGraph_t body = wp.conditional.phGraph_out[0];
+        if (!c->cap_stream) DG_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+        const cudaStream_t main = c->stream;
+        bool split = false;
+        Status hs;
+        DG_CUDA(cudaStreamBeginCaptureToGraph(main, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        dr.fuse_hist = dres;
+        dr.fuse_denom = denom;
+        dr.fuse_hook = [&](const double* xprev, bool* stop) -> Status {
+            *stop = false;
+            cudaStreamCaptureStatus cs;
+            cudaGraph_t cg = nullptr;
+            const cudaGraphNode_t* deps = nullptr;
+            size_t nd = 0;
+            DG_CUDA(cudaStreamGetCaptureInfo(c->stream, &cs, nullptr, &cg, &deps, &nd));
+            cudaGraphConditionalHandle hif;
+            DG_CUDA(cudaGraphConditionalHandleCreate(&hif, cg, 0, cudaGraphCondAssignDefault));
+            DG_TRY(launch(c, kNorms, 0.0, [&] {
+                k_solve_check<<<1, 32, 0, c->stream>>>(nrhs, dres, gst, c->hist_dev, hif, hw);
+            }));
+            DG_TRY(launch(c, kNorms, 16.0 * static_cast<double>(total), [&] {
+                k_copy_lanes_dev<<<grid_for(total, kBlock), kBlock, 0, c->stream>>>(total, nrhs, gst, xprev,
+                                                                                   c->xsol);
+            }));
+            DG_CUDA(cudaStreamGetCaptureInfo(c->stream, &cs, nullptr, &cg, &deps, &nd));
+            cudaGraphNodeParams ip = {};
+            ip.type = cudaGraphNodeTypeConditional;
+            ip.conditional.handle = hif;
+            ip.conditional.type = cudaGraphCondTypeIf;
+            ip.conditional.size = 1;
+            cudaGraphNode_t in;
+            DG_CUDA(cudaGraphAddNode(&in, cg, deps, nd, &ip));
+            DG_CUDA(cudaStreamUpdateCaptureDependencies(c->stream, &in, 1, cudaStreamSetCaptureDependencies));
+            DG_CUDA(cudaStreamBeginCaptureToGraph(c->cap_stream, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                  cudaStreamCaptureModeThreadLocal));
+            c->stream = c->cap_stream;  // the rest of the cycle goes into the IF body
+            split = true;
+            return Status::Ok();
+        };
+        hs = dr.one_cycle(plan);
+        dr.fuse_hook = nullptr;
+        dr.fuse_hist = nullptr;
+        cudaGraph_t tmp = nullptr;
+        if (split) {
+            const cudaError_t e1 = cudaStreamEndCapture(c->cap_stream, &tmp);
+            if (hs.ok() && e1 != cudaSuccess) hs = cuda_status(e1, "graph capture (if body)");
+        }
+        c->stream = main;
+        const cudaError_t e2 = cudaStreamEndCapture(main, &tmp);
+        if (hs.ok() && e2 != cudaSuccess) hs = cuda_status(e2, "graph capture (loop body)");
+        if (hs.ok() && !split) hs = Status::Err(DECMG_RUNTIME, "graph capture: the cycle has no fused residual");
+        if (!hs.ok()) {
+            cudaGraphDestroy(g);
+            return hs;
+        }
+        DG_CUDA(cudaGraphInstantiate(&exec, g, 0));
+        c->graphs.push_back({key, g, exec});
+    }
+    DG_TRY(launch(c, kNorms, 0.0, [&] { k_solve_init<<<1, 1, 0, c->stream>>>(gst, 1, all, max_cycles, tol); }));
+    DG_CUDA(cudaGraphLaunch(exec, c->stream));
+    ++c->launch_count;
+    return Status::Ok();
+}
+
 // A few device scalars -> c->hsmall, written by a kernel through the mapped
 // pinned buffer rather than a copy engine (a 16-double copy would queue behind
 // a concurrent 1.3 GB download in solve_batches), then synchronise.
@@ -304,7 +412,30 @@ Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, co
         }
         return Status::Ok();
     };
-    while (cyc < max_cycles && active) {
+    bool graphed = false;
+    if (c->graph && !c->timing.enabled && max_cycles >= 2 && c->lv.size() > 1) {
+        DG_TRY(dr.one_cycle(plan));  // cycle 0 (from x0; its first sweep carries no residual)
+        cyc = 1;
+        if (dr.can_fuse(plan)) {  // cycles 1.. on the device
+            DG_TRY(solve_graph(c, dr, plan, nrhs, all, tol, max_cycles, denom, dres, total));
+            SolveState st;
+            std::vector<double> hist(static_cast<size_t>(max_cycles) * nrhs);
+            DG_CUDA(cudaMemcpyAsync(&st, c->gstate_raw, sizeof(SolveState), cudaMemcpyDeviceToHost, c->stream));
+            DG_CUDA(cudaMemcpyAsync(hist.data(), c->hist_dev, sizeof(double) * hist.size(), cudaMemcpyDeviceToHost,
+                                    c->stream));
+            DG_CUDA(cudaStreamSynchronize(c->stream));
+            for (int l = 0; l < nrhs; ++l) {
+                done[l] = st.done[l];
+                final_res[l] = st.final_res[l];
+                if (h_hist)
+                    for (int k = 0; k < done[l]; ++k)
+                        h_hist[static_cast<int64_t>(k) * nrhs + l] = hist[static_cast<size_t>(k) * nrhs + l];
+            }
+            active = 0;
+            graphed = true;
+        }
+    }
+    while (!graphed && cyc < max_cycles && active) {
         if (cyc > 0 && dr.can_fuse(plan)) {
             // the first level-0 sweep of the next cycle yields the residual of
             // the current iterate; stop there if every RHS has converged

@@ -120,3 +120,29 @@ def test_solve_batches_equal_single_solves(base, nsub, dirichlet, nrhs):
         np.testing.assert_array_equal(rep.solution, one.solution)
         assert rep.iterations == one.iterations
         assert rep.residual_history == one.residual_history
+
+
+def test_device_solve_loop_matches_host_loop(monkeypatch):
+    """gmg_solve's device-side loop (a CUDA graph: WHILE over one captured
+    cycle with the convergence check and an IF around the rest of the cycle)
+    gives the host-driven loop's iterates, histories and cycle counts, also
+    when calls with different widths, right-hand sides and plans interleave
+    (the graph cache is keyed on them)."""
+    res = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("DECMG_GRAPH", flag)
+        h = d.MultigridHierarchy.from_base("ico", 7, max_nrhs=8)
+        v22 = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+        w11 = d.standard_plan(h.levels(), d.CycleKind.W, 1, 1)
+        out = []
+        for plan, kind, nrhs, seed in [(v22, "uniform", 8, 1), (v22, "uniform", 3, 2), (w11, "lr", 8, 3),
+                                       (v22, "uniform", 8, 4), (v22, "ylm", 1, 5)]:
+            b = h.make_rhs(kind, seed, nrhs) if nrhs > 1 else h.make_rhs(kind, seed)
+            rep = d.gmg_solve(h, plan, b, 1e-9, 40)
+            out.append((rep.solution, rep.iterations, rep.residual_history))
+            plan.cycles = 2
+            out.append((h.run_cycle(plan, b).x, None, None))  # flips no state the next solve depends on
+        res[flag] = out
+    for a, b in zip(res["0"], res["1"]):
+        np.testing.assert_array_equal(a[0], b[0])
+        assert a[1] == b[1] and a[2] == b[2]
