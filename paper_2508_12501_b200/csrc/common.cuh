@@ -208,6 +208,10 @@ struct decmg_gpu_ctx {
     };
     std::vector<GraphEntry> graphs;
     int graph = 1;              // env DECMG_GRAPH=0: host-driven cycle loop
+    // preferred shared-memory carve-out (%) of the row kernels and the projection kernels (env
+    // DECMG_CARVEOUT, -1 = driver default): one common split lets a batch stream's projection blocks share
+    // SMs with the persistent V-cycle kernels instead of holding them until they drain (DESIGN.md §5 x6)
+    int carveout = 50;
     cudaStream_t cap_stream = nullptr;
     double* gstate_raw = nullptr;  // SolveState (rowkernels.cuh) of the device loop
     std::vector<cudaEvent_t> io_events;

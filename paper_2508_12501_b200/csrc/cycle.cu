@@ -114,6 +114,12 @@ Status project_chain_par(decmg_gpu_ctx* c, int nrhs, const double* d_b, int r0, 
         const int smax = kTileRows * 33 * static_cast<int>(sizeof(double));
         DG_CUDA(cudaFuncSetAttribute(k_seq_prod, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
         DG_CUDA(cudaFuncSetAttribute(k_seq_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, kWalkSmem));
+        if (c->carveout >= 0) {
+            DG_CUDA(cudaFuncSetAttribute(k_seq_walk, cudaFuncAttributePreferredSharedMemoryCarveout, c->carveout));
+            DG_CUDA(cudaFuncSetAttribute(k_seq_prod, cudaFuncAttributePreferredSharedMemoryCarveout, c->carveout));
+            DG_CUDA(cudaFuncSetAttribute(k_seq_tree, cudaFuncAttributePreferredSharedMemoryCarveout, c->carveout));
+            DG_CUDA(cudaFuncSetAttribute(k_seq_guess, cudaFuncAttributePreferredSharedMemoryCarveout, c->carveout));
+        }
     }
     double* approx = c->seq_buf;
     double* guess = approx + per;

@@ -62,6 +62,12 @@ struct Driver {
             const bool ell = OP != OP_RESTRICT_RES && (c->kmode == 1 || (c->kmode == 2 && W == 2));
             if (ell) {
                 const unsigned g = grid_for(static_cast<int64_t>(nrows) * (BP / RPT), kBlock);
+                static bool carved = false;
+                if (!carved && c->carveout >= 0) {
+                    cudaFuncSetAttribute(k_rowop_ell<BP, RPT, W, OP>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         c->carveout);
+                    carved = true;
+                }
                 st = launch(c, cls, bytes, [&] { k_rowop_ell<BP, RPT, W, OP><<<g, kBlock, 0, c->stream>>>(a, nrows); });
                 if (grid) *grid = static_cast<int>(g);
             } else {  // persistent pipelined kernel with the TMA-bulk index ring
@@ -74,6 +80,9 @@ struct Driver {
                 if (!attr) {
                     cudaFuncSetAttribute(k_rowop_pipe<BP, RPT, W, OP, W2>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(G::SMEM));
+                    if (c->carveout >= 0)
+                        cudaFuncSetAttribute(k_rowop_pipe<BP, RPT, W, OP, W2>,
+                                             cudaFuncAttributePreferredSharedMemoryCarveout, c->carveout);
                     attr = true;
                 }
                 a.ntiles = ntiles;
@@ -306,6 +315,15 @@ struct Driver {
             const double* b = bptr(k);
             if (L.x_zero) {
                 const double bytes = 8.0 * L.nv + 16.0 * L.nv * R;
+                if (c->carveout >= 0) {
+                    DISPATCH_BP(key, {
+                        static bool carved = false;  // per (BP, RPT)
+                        if (!carved)
+                            cudaFuncSetAttribute(k_sweep_zero<BP, RPT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                 c->carveout);
+                        carved = true;
+                    })
+                }
                 DG_TRY(launch(c, kZeroSweep, bytes, [&] {
                     DISPATCH_BP(key, k_sweep_zero<BP, RPT><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
                                         L.nv, nrhs, L.diag_i, b, xo, plan.omega));

@@ -172,13 +172,13 @@ __global__ void __launch_bounds__(256) k_seq_prod(int r0, int r1, int nrhs, int 
     const int cnt = rows * nrhs;
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
         const int row = q / nrhs, l = q - row * nrhs;
-        tile[row * (nrhs + 1) + l] = __dmul_rn(w[row0 + row], b[base + q]);
+        tile[row * (nrhs + 1) + l] = __dmul_rn(__ldcs(w + row0 + row), __ldcs(b + base + q));
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, t = threadIdx.x & 31;
     for (int l = warp; l < nrhs; l += blockDim.x >> 5) {
         double* dst = prodT + static_cast<int64_t>(l) * stride + (row0 - r0);
-        for (int row = t; row < rows; row += 32) dst[row] = tile[row * (nrhs + 1) + l];
+        for (int row = t; row < rows; row += 32) __stcs(dst + row, tile[row * (nrhs + 1) + l]);
         double s = 0.0;
         for (int i = 0; i < 8; ++i) {
             const int row = t * 8 + i;
@@ -251,6 +251,17 @@ __device__ __forceinline__ SeqNode node_make(const SegFn& f, long long tag) {
     return n;
 }
 
+// Streaming (evict-first) store of a node: the projection runs beside another
+// batch's V-cycle (solve_batches), whose L2-resident data it must not displace.
+__device__ __forceinline__ void st_node(SeqNode* p, const SeqNode& n) {
+    __stcs(&p->lo0, n.lo0);
+    __stcs(&p->hi0, n.hi0);
+    __stcs(&p->d0, n.d0);
+    __stcs(&p->lo1, n.lo1);
+    __stcs(&p->hi1, n.hi1);
+    __stcs(&p->d1, n.d1);
+}
+
 // 3. record functions in their guessed binades and each group's tree of
 // compositions (nodes of 1, 2, 4, ..., 32 records; a node is usable when its
 // records share one binade). grid = (groups of the pass, ceil(nrhs/4)),
@@ -267,7 +278,7 @@ __global__ void __launch_bounds__(128) k_seq_tree(int r0, int r1, int nrhs, int 
     const int rows = min(kGrpRows, r1 - r0 - row0);
     const double* src = prodT + static_cast<int64_t>(l) * stride + row0;
     double* tl = tile[warp];
-    for (int i = t; i < rows; i += 32) tl[(i >> 5) * (kRecRows + 1) + (i & 31)] = src[i];
+    for (int i = t; i < rows; i += 32) tl[(i >> 5) * (kRecRows + 1) + (i & 31)] = __ldcs(src + i);
     __syncwarp();
     const int rec = g * kGrpRecs + t;
     const int rrows = min(kRecRows, rows - t * kRecRows);  // <= 0: padding record
@@ -293,7 +304,7 @@ __global__ void __launch_bounds__(128) k_seq_tree(int r0, int r1, int nrhs, int 
         if (!ok) f = seg_ident();
     }
     SeqNode* out = nodes + (static_cast<int64_t>(l) * kSeqPassGrps + g) * kGrpNodes;
-    out[t] = node_make(f, tag);
+    st_node(out + t, node_make(f, tag));
     for (int lev = 1; lev <= 5; ++lev) {
         const int o = 1 << (lev - 1);
         const SegFn h = seg_shfl_down(f, o);
@@ -301,7 +312,7 @@ __global__ void __launch_bounds__(128) k_seq_tree(int r0, int r1, int nrhs, int 
         if ((t & (2 * o - 1)) == 0) {
             tag = tag_join(tag, th);
             if (tag != kTagNone) f = seg_compose(f, h);
-            out[(64 - (64 >> lev)) + (t >> lev)] = node_make(f, tag);
+            st_node(out + (64 - (64 >> lev)) + (t >> lev), node_make(f, tag));
         }
     }
 }
