@@ -331,24 +331,28 @@ __device__ __forceinline__ bool node_apply(double& s, const SeqNode& n) {
 }
 
 // 4. the exact walk: block l (one warp) = right-hand side l. Every thread
-// carries the same running sum, so control flow is warp-uniform. The warp
-// streams each group's 63 tree nodes and 1024 products into a kWalkStages
-// shared-memory ring with cp.async (16 B per thread per copy; a TMA bulk copy
-// costs ~0.3-1 us of issue per call on one SM, tools/bench_stream1.cu, which
-// would dominate a ~0.5 us group). Per group the warp descends the tree: from
-// each aligned position it tries the largest node, halves on failure, and a
-// single record whose fast path fails is chained literally (__dadd_rn in row
-// order); after a success it climbs back to the largest aligned node, so only
-// the records where the sum crosses a binade (or zero) run element by element.
-constexpr int kWalkStages = 2;
+// carries the same running sum, so control flow is warp-uniform. Groups are
+// walked in batches of 32 whose root nodes (the composition of the whole
+// group) the warp loads one batch ahead; most groups are applied by their root
+// in one step. A group whose root cannot apply -- predicted when the root is
+// empty for both parities (its records straddle a binade or zero), or found
+// when the exact sum misses its interval -- needs its 63-node tree and its
+// 1024 products: predicted groups are prefetched with cp.async into
+// kWalkSlots shared-memory slots as soon as their batch starts, others are
+// fetched on demand into one more slot. Such a group is walked down its tree:
+// from each aligned position the largest node is tried, halved on failure,
+// and a single record whose fast path fails is chained literally (__dadd_rn in
+// row order); after a success the walk climbs back to the largest aligned
+// node, so only the records where the sum crosses a binade (or zero) run
+// element by element.
+constexpr int kWalkSlots = 3;
 constexpr int kWalkNodeBytes = static_cast<int>(sizeof(SeqNode)) * kGrpNodes;  // 3024
 constexpr int kWalkStageBytes = kWalkNodeBytes + 16 + kGrpRows * 8;           // nodes | pad | products
-constexpr int kWalkSmem = kWalkStages * kWalkStageBytes;
+constexpr int kWalkSmem = (kWalkSlots + 1) * kWalkStageBytes + 32 * static_cast<int>(sizeof(SeqNode));
 
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+// mbarrier arrival when all of this thread's earlier cp.async copies have landed
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __global__ void __launch_bounds__(32) k_seq_walk(int r0, int r1, int stride, const double* __restrict__ prodT,
@@ -356,89 +360,138 @@ __global__ void __launch_bounds__(32) k_seq_walk(int r0, int r1, int stride, con
                                                  double total, double* __restrict__ mean_out,
                                                  int* __restrict__ fallbacks) {
     extern __shared__ __align__(128) unsigned char walk_smem[];
+    __shared__ __align__(8) uint64_t bar[kWalkSlots + 1];
+    SeqNode* roots = reinterpret_cast<SeqNode*>(walk_smem + (kWalkSlots + 1) * kWalkStageBytes);
     const int l = blockIdx.x, t = threadIdx.x;
     const int nrows = r1 - r0;
     const int ngrp = (nrows + kGrpRows - 1) / kGrpRows;
-    const unsigned char* ln = reinterpret_cast<const unsigned char*>(nodes + static_cast<int64_t>(l) * kSeqPassGrps * kGrpNodes);
+    const SeqNode* lnode = nodes + static_cast<int64_t>(l) * kSeqPassGrps * kGrpNodes;
+    const unsigned char* ln = reinterpret_cast<const unsigned char*>(lnode);
     const unsigned char* lp = reinterpret_cast<const unsigned char*>(prodT + static_cast<int64_t>(l) * stride);
-    auto issue = [&](int g) {  // every thread; one commit group per call (empty past the end)
-        if (g < ngrp) {
-            unsigned char* base = walk_smem + (g % kWalkStages) * kWalkStageBytes;
-            const unsigned char* ns = ln + static_cast<int64_t>(g) * kWalkNodeBytes;
-            for (int i = t; i < kWalkNodeBytes / 16; i += 32) cp_async16(base + 16 * i, ns + 16 * i);
-            const int rows = min(kGrpRows, nrows - g * kGrpRows);
-            const int nchunk = (rows + 1) >> 1;  // stride is even: 16-byte chunks stay inside the lane
-            const unsigned char* ps = lp + static_cast<int64_t>(g) * kGrpRows * 8;
-            unsigned char* pd = base + kWalkNodeBytes + 16;
-#ifndef SEQ_NOPROD
-            for (int i = t; i < nchunk; i += 32) cp_async16(pd + 16 * i, ps + 16 * i);
-#endif
-        }
-        cp_async_commit();
+    if (t == 0) {
+        for (int i = 0; i <= kWalkSlots; ++i) mbar_init(&bar[i], 32);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    unsigned par = 0;  // phase parity per slot (bit i)
+    // every thread copies its share of group g's nodes and products into slot
+    // sl; the slot's barrier completes when all 32 threads' copies have landed
+    auto fetch = [&](int g, int sl) {
+        unsigned char* base = walk_smem + sl * kWalkStageBytes;
+        const unsigned char* ns = ln + static_cast<int64_t>(g) * kWalkNodeBytes;
+        for (int i = t; i < kWalkNodeBytes / 16; i += 32) cp_async16(base + 16 * i, ns + 16 * i);
+        const int rows = min(kGrpRows, nrows - g * kGrpRows);
+        const int nchunk = (rows + 1) >> 1;  // stride is even: 16-byte chunks stay inside the lane
+        const unsigned char* ps = lp + static_cast<int64_t>(g) * kGrpRows * 8;
+        unsigned char* pd = base + kWalkNodeBytes + 16;
+        for (int i = t; i < nchunk; i += 32) cp_async16(pd + 16 * i, ps + 16 * i);
+        cp_async_mbar_arrive(&bar[sl]);
     };
-#ifdef SEQ_PROFILE
-    const long long c_start = clock64();
-#endif
-    for (int g = 0; g < kWalkStages - 1; ++g) issue(g);
+    auto wait_slot = [&](int sl) {
+        mbar_wait(&bar[sl], (par >> sl) & 1u);
+        par ^= 1u << sl;
+        __syncwarp();
+    };
+    auto load_root = [&](int g, SeqNode& r) {
+        if (g < ngrp) r = lnode[static_cast<int64_t>(g) * kGrpNodes + (kGrpNodes - 1)];
+    };
+    SeqNode rnext;
+    load_root(t, rnext);
     double s = state[l];
     int nfb = 0;
 #ifdef SEQ_PROFILE
+    const long long c_start = clock64();
     long long pw = 0, pt = 0, pl = 0, ntry = 0, pi = 0;
 #endif
-    for (int g = 0; g < ngrp; ++g) {
-        const int st = g % kWalkStages;
-#ifdef SEQ_PROFILE
-        const long long ci = clock64();
-#endif
-        issue(g + kWalkStages - 1);  // into the stage freed at the end of group g-1
-#ifdef SEQ_PROFILE
-        const long long c0 = clock64();
-        pi += c0 - ci;
-#endif
-        cp_async_wait<kWalkStages - 1>();
+    int slot_grp[kWalkSlots];
+#pragma unroll
+    for (int i = 0; i < kWalkSlots; ++i) slot_grp[i] = -1;
+    for (int g0 = 0; g0 < ngrp; g0 += 32) {
         __syncwarp();
+        roots[t] = rnext;
+        __syncwarp();
+        load_root(g0 + 32 + t, rnext);  // next batch, in flight during this one
+        const double inf = __longlong_as_double(0x7ff0000000000000ll);
+        const bool pred = g0 + t < ngrp && roots[t].lo0 == inf && roots[t].lo1 == inf;
+        unsigned pend = __ballot_sync(0xffffffffu, pred);  // predicted crossings not yet prefetched
+#pragma unroll
+        for (int i = 0; i < kWalkSlots; ++i)
+            if (pend) {
+                const int g = g0 + __ffs(pend) - 1;
+                pend &= pend - 1;
+                fetch(g, i);
+                slot_grp[i] = g;
+            }
+        const int jb = min(32, ngrp - g0);
+        for (int k = 0; k < jb; ++k) {
+            const int g = g0 + k;
 #ifdef SEQ_PROFILE
-        pw += clock64() - c0;
+            ++ntry;
 #endif
-        const SeqNode* nd = reinterpret_cast<const SeqNode*>(walk_smem + st * kWalkStageBytes);
-        const double* pr = reinterpret_cast<const double*>(walk_smem + st * kWalkStageBytes + kWalkNodeBytes + 16);
-        const int rows = min(kGrpRows, nrows - g * kGrpRows);
-        const int jn = (rows + kRecRows - 1) / kRecRows;
-        int pos = 0;
-        while (pos < jn) {
-            int lev = pos ? min(5, __ffs(pos) - 1) : 5;
-            for (;;) {
+            if (node_apply(s, roots[k])) continue;
+            int sl = kWalkSlots;  // the demand slot unless prefetched
+#pragma unroll
+            for (int i = 0; i < kWalkSlots; ++i)
+                if (slot_grp[i] == g) sl = i;
 #ifdef SEQ_PROFILE
-                ++ntry;
-                const long long c2 = clock64();
-                const bool okk = node_apply(s, nd[(64 - (64 >> lev)) + (pos >> lev)]);
-                pt += clock64() - c2;
-                if (okk) {
-#else
-                if (node_apply(s, nd[(64 - (64 >> lev)) + (pos >> lev)])) {
+            const long long c0 = clock64();
 #endif
-                    pos += 1 << lev;
+            if (sl == kWalkSlots) fetch(g, sl);
+            wait_slot(sl);
+#ifdef SEQ_PROFILE
+            pw += clock64() - c0;
+#endif
+            const SeqNode* nd = reinterpret_cast<const SeqNode*>(walk_smem + sl * kWalkStageBytes);
+            const double* pr = reinterpret_cast<const double*>(walk_smem + sl * kWalkStageBytes + kWalkNodeBytes + 16);
+            const int rows = min(kGrpRows, nrows - g * kGrpRows);
+            const int jn = (rows + kRecRows - 1) / kRecRows;
+            int pos = 0;
+            while (pos < jn) {
+                int lev = pos ? min(4, __ffs(pos) - 1) : 4;  // the root (level 5) already failed
+                for (;;) {
+#ifdef SEQ_PROFILE
+                    ++ntry;
+#endif
+                    if (node_apply(s, nd[(64 - (64 >> lev)) + (pos >> lev)])) {
+                        pos += 1 << lev;
+                        break;
+                    }
+                    if (lev > 0) {
+                        --lev;
+                        continue;
+                    }
+                    ++nfb;  // the literal chain over record pos
+#ifdef SEQ_PROFILE
+                    const long long c3 = clock64();
+#endif
+                    const int rr = min(kRecRows, rows - pos * kRecRows);
+                    const double* p = pr + pos * kRecRows;
+                    for (int i = 0; i < rr; ++i) s = __dadd_rn(s, p[i]);
+#ifdef SEQ_PROFILE
+                    pl += clock64() - c3;
+#endif
+                    pos += 1;
                     break;
                 }
-                if (lev > 0) {
-                    --lev;
-                    continue;
+            }
+            __syncwarp();
+            if (sl < kWalkSlots) {  // slot free: prefetch the batch's next predicted crossing
+                slot_grp[sl] = -1;
+                if (pend) {
+                    const int g2 = g0 + __ffs(pend) - 1;
+                    pend &= pend - 1;
+                    fetch(g2, sl);
+                    slot_grp[sl] = g2;
                 }
-                ++nfb;  // the literal chain over record pos
-#ifdef SEQ_PROFILE
-                const long long c3 = clock64();
-#endif
-                const int rr = min(kRecRows, rows - pos * kRecRows);
-                const double* p = pr + pos * kRecRows;
-                for (int i = 0; i < rr; ++i) s = __dadd_rn(s, p[i]);
-#ifdef SEQ_PROFILE
-                pl += clock64() - c3;
-#endif
-                pos += 1;
-                break;
             }
         }
-        __syncwarp();
+        // prefetched groups whose root applied after all: retire their copies
+#pragma unroll
+        for (int i = 0; i < kWalkSlots; ++i)
+            if (slot_grp[i] >= 0) {
+                wait_slot(i);
+                slot_grp[i] = -1;
+            }
     }
     if (t == 0) {
         state[l] = s;
