@@ -272,9 +272,14 @@ int decmg_gpu_pcg(decmg_gpu_ctx* ctx, const decmg_gpu_plan* inner, int inner_cyc
     if (nrhs < 1 || nrhs > ctx->max_nrhs)
         return fail(ctx, Status::Err(DECMG_INVALID_ARGUMENT, "nrhs must be in [1, max_nrhs]"));
     const size_t n = static_cast<size_t>(ctx->lv[0].nv) * nrhs;
-    API_TRY(ctx, cuda_status(cudaMemcpyAsync(ctx->io_b, b, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D b"));
-    API_TRY(ctx, pcg(ctx, p, inner_cycles, nrhs, ctx->io_b, tol, maxiter, ctx->io_x, hist_out, iters_out,
-                     converged_out, final_out));
+    if (ctx->dirichlet)
+        return fail(ctx, Status::Err(DECMG_INVALID_ARGUMENT,
+                                     "gmg_pcg: Neumann hierarchies only (the reference projects b)"));
+    (void)n;
+    // H2D of b overlapped with the projection chain (stage_rhs), into ctx->bproj
+    API_TRY(ctx, stage_rhs(ctx, nrhs, b, true));
+    API_TRY(ctx, pcg(ctx, p, inner_cycles, nrhs, nullptr, tol, maxiter, ctx->io_x, hist_out, iters_out,
+                     converged_out, final_out, true));
     if (x_out)
         API_TRY(ctx, cuda_status(cudaMemcpyAsync(x_out, ctx->io_x, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H x"));
     API_TRY(ctx, cuda_status(cudaStreamSynchronize(ctx->stream), "gmg_pcg"));

@@ -294,7 +294,7 @@ Status solve_batches(decmg_gpu_ctx* c, const Plan& plan, int nrhs, int nbatch, c
                      int max_cycles, double* const* h_x, double* h_hist, int* cycles_done, double* h_final);
 // pcg.cu: gmg_preconditioned_cg (proj/src/solvers.cpp:118-130)
 Status pcg(decmg_gpu_ctx* c, const Plan& inner, int inner_cycles, int nrhs, const double* d_b, double tol,
-           int maxiter, double* d_x, double* h_hist, int* iters, int* converged, double* h_final);
+           int maxiter, double* d_x, double* h_hist, int* iters, int* converged, double* h_final, bool staged = false);
 Status project_compatible(decmg_gpu_ctx* c, int nrhs, double* d_b);
 Status apply_op(decmg_gpu_ctx* c, int level, char op, const double* d_x, double* d_y);
 

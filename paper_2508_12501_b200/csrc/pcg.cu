@@ -20,7 +20,7 @@
 namespace decmg_gpu {
 
 Status pcg(decmg_gpu_ctx* c, const Plan& inner, int inner_cycles, int nrhs, const double* d_b, double tol,
-           int maxiter, double* d_x, double* h_hist, int* iters, int* converged, double* h_final) {
+           int maxiter, double* d_x, double* h_hist, int* iters, int* converged, double* h_final, bool staged) {
     DG_TRY(check_nrhs(c, nrhs));
     if (c->dirichlet)
         return Status::Err(DECMG_INVALID_ARGUMENT, "gmg_pcg: Neumann hierarchies only (the reference projects b)");
@@ -48,9 +48,12 @@ Status pcg(decmg_gpu_ctx* c, const Plan& inner, int inner_cycles, int nrhs, cons
     const size_t vb = sizeof(double) * static_cast<size_t>(n) * nrhs;
     cudaStream_t st = c->stream;
 
-    // bc = project_compatible(b) (reference numbering), then internal
-    DG_CUDA(cudaMemcpyAsync(c->bproj, d_b, vb, cudaMemcpyDeviceToDevice, st));
-    DG_TRY(project_compatible(c, nrhs, c->bproj));
+    // bc = project_compatible(b) (reference numbering), then internal; staged:
+    // stage_rhs already left the projected right-hand side in c->bproj
+    if (!staged) {
+        DG_CUDA(cudaMemcpyAsync(c->bproj, d_b, vb, cudaMemcpyDeviceToDevice, st));
+        DG_TRY(project_compatible(c, nrhs, c->bproj));
+    }
     Driver dr{c, nrhs, bp_of(nrhs), r};
     dr.init();
     DG_TRY(dr.to_internal(c->bproj, bc));
@@ -104,7 +107,9 @@ Status pcg(decmg_gpu_ctx* c, const Plan& inner, int inner_cycles, int nrhs, cons
     DG_CUDA(cudaMemcpyAsync(p, z, vb, cudaMemcpyDeviceToDevice, st));
     DG_TRY(wdot(r, z, rz));
     DG_TRY(norm(r, res, 2, denom));
-    std::vector<double> hres(nrhs), hc(nrhs), ha(nrhs);
+    std::vector<double> hres(nrhs), hres_g(34);
+    double* guard = res + 32;  // [kind, iteration] of the first breakdown (pcg_s + 224)
+    DG_CUDA(cudaMemsetAsync(guard, 0, sizeof(double) * 2, st));
     DG_TRY(fetch(res, hres));
     unsigned active = 0;
     for (int l = 0; l < nrhs; ++l) {
@@ -119,15 +124,8 @@ Status pcg(decmg_gpu_ctx* c, const Plan& inner, int inner_cycles, int nrhs, cons
         DG_TRY(apply(p, ap));
         DG_TRY(wdot(p, ap, curv));
         DG_TRY(launch(c, kNorms, 0.0, [&] { k_lane_div<<<1, 32, 0, st>>>(nrhs, rz, curv, alpha); }));
-        DG_TRY(fetch(curv, hc));
-        DG_TRY(fetch(alpha, ha));
-        for (int l = 0; l < nrhs; ++l) {
-            if (!(active & (1u << l))) continue;
-            if (hc[l] == 0.0 || !std::isfinite(hc[l]))
-                return Status::Err(DECMG_RUNTIME, "cg: breakdown (zero curvature) at iteration " + std::to_string(it));
-            if (!std::isfinite(ha[l]))
-                return Status::Err(DECMG_RUNTIME, "cg: breakdown (non-finite step) at iteration " + std::to_string(it));
-        }
+        // breakdown checks (solvers.cpp) on the device, read with this iteration's residuals
+        DG_TRY(launch(c, kNorms, 0.0, [&] { k_pcg_guard<<<1, 32, 0, st>>>(nrhs, active, it, curv, alpha, guard); }));
         DG_TRY(launch(c, kNorms, 48.0 * n * nrhs, [&] {
             DISPATCH_BP(dr.key, k_cg_xr<BP, RPT><<<g, kBlock, 0, st>>>(n, nrhs, alpha, active, x, r, p, ap));
         }));
@@ -140,7 +138,13 @@ Status pcg(decmg_gpu_ctx* c, const Plan& inner, int inner_cycles, int nrhs, cons
         }));
         ++it;
         DG_TRY(norm(r, res, 2, denom));
-        DG_TRY(fetch(res, hres));
+        DG_CUDA(cudaMemcpyAsync(hres_g.data(), res, sizeof(double) * 34, cudaMemcpyDeviceToHost, st));
+        DG_CUDA(cudaStreamSynchronize(st));
+        if (hres_g[32] != 0.0)
+            return Status::Err(DECMG_RUNTIME, std::string(hres_g[32] == 1.0 ? "cg: breakdown (zero curvature)"
+                                                                           : "cg: breakdown (non-finite step)") +
+                                                  " at iteration " + std::to_string(static_cast<int>(hres_g[33])));
+        for (int l = 0; l < nrhs; ++l) hres[l] = hres_g[l];
         for (int l = 0; l < nrhs; ++l) {
             if (!(active & (1u << l))) continue;
             if (h_hist) h_hist[static_cast<size_t>(it) * nrhs + l] = hres[l];
