@@ -146,3 +146,25 @@ def test_device_solve_loop_matches_host_loop(monkeypatch):
     for a, b in zip(res["0"], res["1"]):
         np.testing.assert_array_equal(a[0], b[0])
         assert a[1] == b[1] and a[2] == b[2]
+
+
+def test_solve_batches_edges():
+    """Batch streams: no batches, a cycle cap of 0 (the solution is x0 = 0 and
+    the residual is reported) and of 1, and a null right-hand side."""
+    h = d.MultigridHierarchy.from_base("ico", 5, max_nrhs=2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    assert d.gmg_solve_batches(h, plan, [], 1e-8, 10) == []
+    b = h.make_rhs("uniform", 2, 2)
+    for cap in (0, 1):
+        rep = d.gmg_solve_batches(h, plan, [b, b], 1e-8, cap)
+        one = d.gmg_solve(h, plan, b, 1e-8, cap)
+        for r in rep:
+            np.testing.assert_array_equal(r.solution, one.solution)
+            assert r.iterations == one.iterations
+            assert r.final_relative_residual == one.final_relative_residual
+    import ctypes as C
+    from paper_2508_12501_b200.multigrid import _plan_struct
+    ps, keep = _plan_struct(plan, h.levels())
+    ptrs = (C.c_void_p * 1)(None)
+    rc = h._lib.decmg_gpu_solve_batches(h.ctx, C.byref(ps), 2, 1, ptrs, 1e-8, 10, ptrs, None, None, None)
+    assert rc == 1  # DECMG_INVALID_ARGUMENT
