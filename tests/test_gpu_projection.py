@@ -44,7 +44,7 @@ def check(h, o, B):
     np.testing.assert_array_equal(got.view(np.uint64), ref.view(np.uint64))
 
 
-@pytest.mark.parametrize("base,nsub", [("ico", 6), ("square", 7)])
+@pytest.mark.parametrize("base,nsub", [("ico", 6), ("square", 7), ("ico", 1), ("square", 2)])
 @pytest.mark.parametrize("kind", ["uniform", "positive", "wide", "ties", "zeros_spikes"])
 def test_projection_bit_exact(base, nsub, kind):
     nrhs = 5
