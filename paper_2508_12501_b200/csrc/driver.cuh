@@ -80,7 +80,10 @@ struct Driver {
                 if (!attr) {
                     cudaFuncSetAttribute(k_rowop_pipe<BP, RPT, W, OP, W2>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(G::SMEM));
-                    if (c->carveout >= 0)
+                    // the common carve-out only where all per_sm CTAs still fit in it (the
+                    // single-RHS tiles need ~80 KB each: the driver's choice keeps them resident)
+                    if (c->carveout >= 0 &&
+                        per_sm * (G::SMEM + 1024.0) <= c->carveout / 100.0 * kSmemPerSm)
                         cudaFuncSetAttribute(k_rowop_pipe<BP, RPT, W, OP, W2>,
                                              cudaFuncAttributePreferredSharedMemoryCarveout, c->carveout);
                     attr = true;
