@@ -79,18 +79,18 @@ struct Driver {
                 static bool attr = false;
                 if (!attr) {
                     cudaFuncSetAttribute(k_rowop_pipe<BP, RPT, W, OP, W2>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(G::SMEM));
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(G::PSMEM));
                     // the common carve-out only where all per_sm CTAs still fit in it (the
                     // single-RHS tiles need ~80 KB each: the driver's choice keeps them resident)
                     if (c->carveout >= 0 &&
-                        per_sm * (G::SMEM + 1024.0) <= c->carveout / 100.0 * kSmemPerSm)
+                        per_sm * (G::PSMEM + 1024.0) <= c->carveout / 100.0 * kSmemPerSm)
                         cudaFuncSetAttribute(k_rowop_pipe<BP, RPT, W, OP, W2>,
                                              cudaFuncAttributePreferredSharedMemoryCarveout, c->carveout);
                     attr = true;
                 }
                 a.ntiles = ntiles;
                 st = launch(c, cls, bytes, [&] {
-                    k_rowop_pipe<BP, RPT, W, OP, W2><<<g, kPipeThreads, G::SMEM, c->stream>>>(a);
+                    k_rowop_pipe<BP, RPT, W, OP, W2><<<g, kPipeThreads, G::PSMEM, c->stream>>>(a);
                 });
                 if (grid) *grid = g;
             }

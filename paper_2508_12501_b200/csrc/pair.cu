@@ -305,11 +305,11 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_rowop_pair(Pai
                 else if (BP * 8 >= 128) ldv<RPT>(a.xp + o, xr);
                 else ldv_cg<RPT>(a.xp + o, xr);
             }
+            const double y = active ? div_seed(d) : 0.0;  // consumes the stage's d before the release
             __syncwarp();
             if ((tid & 31) == 0) mbar_arrive(&empty[s]);  // stage consumed
             if (active) {
                 double res[RPT];
-                const double y = div_seed(d);
 #pragma unroll
                 for (int l = 0; l < RPT; ++l) {
                     if constexpr (NORM) {
