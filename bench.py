@@ -17,6 +17,12 @@ grouped send/recv, coarse levels replicated) -- strong
 scaling of the fixed problem; the cycle time is the max over ranks.
 `--impl reference` times the reference's CPU solver (oracle/_ref, the
 reference compiled in place) on a bounded sample on the host cores.
+
+Besides the headline: `roofline` (the level-0 sweep kernel against the
+measured HBM peak), `cycle_roofline` (the whole cycle's compulsory bytes per
+SURVEY.md 8(d)), and `e2e` -- K gmg_solve steps of the 16-RHS batch from and
+to pinned host memory through the batch stream API (decmg_gpu_solve_batches),
+with one isolated call's time to 1e-8 beside it.
 """
 from __future__ import annotations
 
