@@ -48,6 +48,8 @@ Status init_ctx(decmg_gpu_ctx* c, const decmg_gpu_config* cfg) {
     if (const char* e = std::getenv("DECMG_PAIR")) c->pair = std::atoi(e) != 0;
     if (const char* e = std::getenv("DECMG_GRAPH")) c->graph = std::atoi(e) != 0;
     if (const char* e = std::getenv("DECMG_CARVEOUT")) c->carveout = std::atoi(e);
+    if (const char* e = std::getenv("DECMG_VTAIL")) c->vtail = std::atoi(e) != 0;
+    if (const char* e = std::getenv("DECMG_VTAIL_ITEMS")) c->vtail_items = std::atoll(e);
     if (const char* e = std::getenv("DECMG_PAIR_CH")) c->pair_ch = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("DECMG_PAIR_LAG")) c->pair_lag = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("DECMG_PFL")) c->pfl = std::atoi(e);

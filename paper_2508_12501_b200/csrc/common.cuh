@@ -212,6 +212,8 @@ struct decmg_gpu_ctx {
     // DECMG_CARVEOUT, -1 = driver default): one common split lets a batch stream's projection blocks share
     // SMs with the persistent V-cycle kernels instead of holding them until they drain (DESIGN.md §5 x6)
     int carveout = 50;
+    int vtail = 1;              // bottom of the V in one cooperative kernel (env DECMG_VTAIL=0: per-pass kernels)
+    int64_t vtail_items = 262144;  // ... from the first level with at most this many rows x RHS (env DECMG_VTAIL_ITEMS)
     cudaStream_t cap_stream = nullptr;
     double* gstate_raw = nullptr;  // SolveState (rowkernels.cuh) of the device loop
     std::vector<cudaEvent_t> io_events;

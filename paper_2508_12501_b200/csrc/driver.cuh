@@ -489,12 +489,116 @@ struct Driver {
         return Status::Ok();
     }
 
+    // The bottom of a V from `level` (walk[w] == 'd') in one cooperative kernel
+    // (rowkernels.cuh k_vtail) when every pass below is small: the walk from w
+    // must be d^m u^m down to the coarsest, Jacobi, ELL operators everywhere,
+    // at least one pre-sweep per level. Returns false (nothing launched) if not.
+    bool tail_ok(const Plan& plan, int w, int level) const {
+        const int Lc = static_cast<int>(c->lv.size());
+        const int m = Lc - 1 - level;
+        if (!c->vtail || level < 1 || m < 1 || m >= kTailMax || tpr > 8 || fuse_hist) return false;
+        if (plan.smoother != DECMG_SMOOTHER_JACOBI || c->pair) return false;
+        if (static_cast<int64_t>(c->lv[level].nv) * nrhs > c->vtail_items) return false;
+        if (w + 2 * m > static_cast<int>(plan.walk.size())) return false;
+        for (int i = 0; i < m; ++i)
+            if (plan.walk[w + i] != 'd' || plan.walk[w + m + i] != 'u') return false;
+        for (int k = level; k < Lc - 1; ++k) {
+            const Level& L = c->lv[k];
+            if (!L.Le_ci || !L.Re_ci || !L.Pe_ci || !L.Le_row || !L.Re_row || plan.pre[k] < 1 ||
+                L.zero_diag_row >= 0)
+                return false;
+        }
+        return true;
+    }
+
+    Status run_tail(const Plan& plan, int level) {
+        const int Lc = static_cast<int>(c->lv.size());
+        const int nl = Lc - level;
+        TailArgs a{};
+        a.nl = nl;
+        a.nrhs = nrhs;
+        a.project = c->dirichlet ? 0 : 1;
+        a.omega = plan.omega;
+        a.r = c->r;
+        const Level& Cst = c->lv[Lc - 1];
+        a.crp = Cst.L_rp;
+        a.cci = Cst.L_ci;
+        a.cv = Cst.L_v;
+        a.carea = Cst.area;
+        a.cwtot = Cst.wtot;
+        a.cscratch = c->coarse_scratch;
+        for (int i = 0; i < nl; ++i) {
+            const Level& L = c->lv[level + i];
+            TailLevel& T = a.lv[i];
+            T.nv = L.nv;
+            T.Lw = L.Le_w;
+            T.Rw = L.Re_w;
+            T.pre = plan.pre[level + i];
+            T.post = plan.post[level + i];
+            T.cur = L.cur;
+            T.xzero = L.x_zero ? 1 : 0;
+            T.Lci = L.Le_ci;
+            T.Lv = L.Le_v;
+            T.Lrow = L.Le_row;
+            T.Rci = L.Re_ci;
+            T.Rv = L.Re_v;
+            T.Rrow = L.Re_row;
+            T.Pci = L.Pe_ci;
+            T.Pv = L.Pe_v;
+            T.diag = L.diag_i;
+            T.bdc = (c->dirichlet && i + 1 < nl) ? c->lv[level + i + 1].bd_i : nullptr;
+            T.x[0] = L.x[0];
+            T.x[1] = L.x[1];
+            T.b = const_cast<double*>(bptr(level + i));
+        }
+        Status st;
+        DISPATCH_BP(key, {
+            auto kern = k_vtail<BP, RPT>;
+            static int blocks = -1;
+            if (blocks < 0) {
+                int nb = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kBlock, 0);
+                blocks = nb >= 1 ? c->num_sms : 0;
+            }
+            if (blocks == 0) {
+                st = Status::Err(DECMG_CUDA, "bottom-of-V kernel does not fit on an SM");
+            } else {
+                st = launch(c, kCoarseLevels, 0.0, [&] {
+                    cudaLaunchConfig_t cfg = {};
+                    cfg.gridDim = dim3(blocks);
+                    cfg.blockDim = dim3(kBlock);
+                    cfg.dynamicSmemBytes = 0;
+                    cfg.stream = c->stream;
+                    cudaLaunchAttribute at[1];
+                    at[0].id = cudaLaunchAttributeCooperative;
+                    at[0].val.cooperative = 1;
+                    cfg.attrs = at;
+                    cfg.numAttrs = 1;
+                    cudaLaunchKernelEx(&cfg, kern, a);
+                });
+            }
+        })
+        DG_TRY(st);
+        // the host's view of the levels after the tail: each sweep flipped the ping-pong buffer
+        for (int i = 0; i < nl; ++i) {
+            Level& L = c->lv[level + i];
+            if (i + 1 < nl) L.cur ^= (plan.pre[level + i] + plan.post[level + i]) & 1;
+            L.x_zero = false;
+        }
+        return Status::Ok();
+    }
+
     // MultigridHierarchy::cycle_once (multigrid.cpp:252-285)
     Status cycle_once(const Plan& plan) {
         const int nw = static_cast<int>(plan.walk.size());
         const int Lc = static_cast<int>(c->lv.size());
         int level = 0;
         for (int w = 0; w < nw; ++w) {
+            if (plan.walk[w] == 'd' && tail_ok(plan, w, level)) {
+                DG_TRY(run_tail(plan, level));
+                w += 2 * (Lc - 1 - level) - 1;  // the walk resumes with the 'u' out of `level`
+                continue;
+            }
             if (plan.walk[w] == 'd') {
                 DG_TRY(smooth(level, plan.pre[level], plan));
                 if (stopped) return Status::Ok();
