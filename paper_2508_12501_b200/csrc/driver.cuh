@@ -482,8 +482,12 @@ struct Driver {
         const double* b = bptr(k);
         const int project = c->dirichlet ? 0 : 1;
         DG_TRY(launch(c, kCoarseSolve, 0.0, [&] {
-            k_coarse_cg<<<1, 32, 0, c->stream>>>(L.nv, nrhs, L.L_rp, L.L_ci, L.L_v, L.area, L.wtot,
-                                                 project, b, x, c->coarse_scratch);
+            if (L.nv <= 32)  // one warp per right-hand side
+                k_coarse_cg_warp<<<(nrhs + 7) / 8, 256, 0, c->stream>>>(L.nv, nrhs, L.L_rp, L.L_ci, L.L_v, L.area,
+                                                                         L.wtot, project, b, x);
+            else
+                k_coarse_cg<<<1, 32, 0, c->stream>>>(L.nv, nrhs, L.L_rp, L.L_ci, L.L_v, L.area, L.wtot,
+                                                     project, b, x, c->coarse_scratch);
         }));
         L.x_zero = false;
         return Status::Ok();
