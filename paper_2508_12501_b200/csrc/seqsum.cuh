@@ -466,7 +466,15 @@ __global__ void __launch_bounds__(32) k_seq_walk(int r0, int r1, int stride, con
 #endif
                     const int rr = min(kRecRows, rows - pos * kRecRows);
                     const double* p = pr + pos * kRecRows;
-                    for (int i = 0; i < rr; ++i) s = __dadd_rn(s, p[i]);
+                    if (rr == kRecRows) {  // full record: operands in registers first, then the add chain
+                        double q[kRecRows];
+#pragma unroll
+                        for (int i = 0; i < kRecRows; ++i) q[i] = p[i];
+#pragma unroll
+                        for (int i = 0; i < kRecRows; ++i) s = __dadd_rn(s, q[i]);
+                    } else {
+                        for (int i = 0; i < rr; ++i) s = __dadd_rn(s, p[i]);
+                    }
 #ifdef SEQ_PROFILE
                     pl += clock64() - c3;
 #endif
