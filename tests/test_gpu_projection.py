@@ -168,3 +168,28 @@ def test_solve_batches_edges():
     ptrs = (C.c_void_p * 1)(None)
     rc = h._lib.decmg_gpu_solve_batches(h.ctx, C.byref(ps), 2, 1, ptrs, 1e-8, 10, ptrs, None, None, None)
     assert rc == 1  # DECMG_INVALID_ARGUMENT
+
+
+@pytest.mark.parametrize("base,nsub,dirichlet,nrhs,kind", [("ico", 7, False, 16, "V"), ("ico", 6, False, 5, "W"),
+                                                           ("square", 7, True, 1, "F"), ("square", 6, True, 3, "V")])
+def test_bottom_of_v_kernel_bitwise(monkeypatch, base, nsub, dirichlet, nrhs, kind):
+    """The cooperative bottom-of-V kernel (k_vtail, DECMG_VTAIL=1, default)
+    gives the per-pass kernels' iterates bit for bit for V, W and F walks,
+    Neumann and Dirichlet, 1-16 right-hand sides, from a threshold that puts
+    every level but the finest into it."""
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("DECMG_VTAIL", flag)
+        monkeypatch.setenv("DECMG_VTAIL_ITEMS", "100000000")
+        h = d.MultigridHierarchy.from_base(base, nsub, dirichlet=dirichlet, max_nrhs=nrhs)
+        b = h.make_rhs("uniform", 6, nrhs) if nrhs > 1 else h.make_rhs("uniform", 6)
+        if not dirichlet:
+            b = h.project_compatible(b)
+        plan = d.standard_plan(h.levels(), getattr(d.CycleKind, kind), 2, 2)
+        plan.cycles = 3
+        res = h.run_cycle(plan, b)
+        rep = d.gmg_solve(h, plan, b, 1e-9, 30)
+        out[flag] = (res.x, rep.solution, rep.iterations)
+    np.testing.assert_array_equal(out["1"][0], out["0"][0])
+    np.testing.assert_array_equal(out["1"][1], out["0"][1])
+    assert out["1"][2] == out["0"][2]
