@@ -203,7 +203,7 @@ def run_ours(args, world, rank, local):
     n = h.n()
     levels = h.levels()
     lib = _lib.load()
-    plan = d.standard_plan(levels, d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(levels, d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     ps, keep = _plan_struct(plan, levels)
 
     B = h.make_rhs("uniform", SEED0 + args.nrhs * rank, args.nrhs)  # [n][nrhs], seeds s0..s0+15
@@ -377,7 +377,7 @@ def run_partitioned(args, world, rank, local):
     g = dh.context()
     n = g.n()
     levels = dh.levels()
-    plan = d.standard_plan(levels, d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(levels, d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     B = g.make_rhs("uniform", SEED0, args.nrhs)  # the same batch as the 1-GPU run
     Bp = g.project_compatible(B)
     hb = torch.from_numpy(Bp).pin_memory().numpy()
@@ -406,10 +406,10 @@ def run_partitioned(args, world, rank, local):
                 "algorithmic_bytes_per_launch": tbytes / max(nl, 1), "launches": nl}
     # e2e: gmg_solve to 1e-8 from pinned host memory to pinned host memory
     hB = torch.from_numpy(B).pin_memory().numpy()
-    dh.gmg_solve(d.standard_plan(levels, d.CycleKind.V, 2, 2), hB, 1e-8, 200)
+    dh.gmg_solve(d.standard_plan(levels, d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi)), hB, 1e-8, 200)
     barrier(world)
     t0 = time.perf_counter()
-    rep = dh.gmg_solve(d.standard_plan(levels, d.CycleKind.V, 2, 2), hB, 1e-8, 200)
+    rep = dh.gmg_solve(d.standard_plan(levels, d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi)), hB, 1e-8, 200)
     e2e_s = max_over_ranks(world, time.perf_counter() - t0)
     cyc = sum(rep.iterations)
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -96,7 +96,9 @@ DECMG_API int decmg_gpu_create_from_levels(const decmg_gpu_level_desc* levels, i
 DECMG_API void decmg_gpu_destroy(decmg_gpu_ctx* ctx);
 DECMG_API const char* decmg_gpu_last_error(const decmg_gpu_ctx* ctx);
 
-/* CyclePlan (proj/include/decmg/multigrid.hpp:70-89). walk: 'd'/'u' string
+/* CyclePlan (proj/include/decmg/multigrid.hpp:70-89); a NULL plan pointer is
+ * standard_plan(levels, CycleKind::V) with the reference defaults (V(3,3),
+ * Gauss-Seidel, multigrid.hpp:58,88-89). walk: 'd'/'u' string
  * (NULL = the V walk of standard_plan, multigrid.cpp:171-194); pre/post:
  * per-level sweep counts (NULL = pre_all/post_all on every level).
  * smoother (SmootherConfig, multigrid.hpp:55-60; smooth, multigrid.cpp:95-120):

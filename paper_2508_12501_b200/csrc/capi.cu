@@ -40,18 +40,12 @@ Status init_ctx(decmg_gpu_ctx* c, const decmg_gpu_config* cfg) {
     DG_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     DG_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi));
     DG_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
-    if (const char* e = std::getenv("DECMG_SWEEP2")) c->sweep2 = std::atoi(e) != 0;
     if (const char* e = std::getenv("DECMG_PF")) c->pf = std::atoi(e);
-    if (const char* e = std::getenv("DECMG_FUSE_RR")) c->fuse_rr = std::atoi(e) != 0;
-    if (const char* e = std::getenv("DECMG_RR_WINDOW")) c->rr_window = std::atoi(e) != 0;
     if (const char* e = std::getenv("DECMG_PROJ_SEQ")) c->proj_seq = std::atoi(e) != 0;
-    if (const char* e = std::getenv("DECMG_PAIR")) c->pair = std::atoi(e) != 0;
     if (const char* e = std::getenv("DECMG_GRAPH")) c->graph = std::atoi(e) != 0;
     if (const char* e = std::getenv("DECMG_CARVEOUT")) c->carveout = std::atoi(e);
     if (const char* e = std::getenv("DECMG_VTAIL")) c->vtail = std::atoi(e) != 0;
     if (const char* e = std::getenv("DECMG_VTAIL_ITEMS")) c->vtail_items = std::atoll(e);
-    if (const char* e = std::getenv("DECMG_PAIR_CH")) c->pair_ch = std::max(1, std::atoi(e));
-    if (const char* e = std::getenv("DECMG_PAIR_LAG")) c->pair_lag = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("DECMG_PFL")) c->pfl = std::atoi(e);
     if (const char* e = std::getenv("DECMG_KERNEL")) {
         const std::string m(e);

@@ -10,7 +10,11 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <set>
 #include <string>
+#include <tuple>
 #include <utility>
 #include <vector>
 
@@ -108,29 +112,9 @@ struct Level {
     int Le_w = 0;            // ELL widths (7 or 8; 0 = no ELL copy)
     int Re_w = 0;
     int* Le_row = nullptr;   // row q | diag slot << kRowBits per ELL row of Le/Pe (-1 = padding)
-    // Fused sweep pairs (k_sweep2): tiles of kS2Rows consecutive ELL rows; for
-    // each tile the ELL rows of its 1-ring halo, and per ELL entry the slot of
-    // its column in the tile's shared-memory vector (tile rows, then halo).
-    int* S2_hptr = nullptr;  // [ntiles+1]
-    int* S2_halo = nullptr;  // ELL row indices of halo rows
-    int* S2_slot = nullptr;  // [npad * Le_w]
-    int S2_maxhalo = -1;     // -1: no tiles
-    // Wavefront sweep pairs (pair.cu): per 56-row ELL tile its neighbour tiles,
-    // sweep-1 completion counters (epoch-based, never reset) and a completed-tile count.
-    int* pr_deps = nullptr;
-    unsigned* pr_flags = nullptr;
-    unsigned long long* pr_done = nullptr;
-    unsigned pr_epoch = 0;
-    int pr_rows = 0;
     // Exact lexicographic Gauss-Seidel as a level schedule (setup.cu
     // build_gs_schedule): phase p of the forward (f) / reverse (r) sweep is
     // the internal rows gs?_rows[gs?_ptr[p] .. gs?_ptr[p+1]), ascending.
-    // Fused residual + restriction (rowkernels.cuh k_res_restrict): coarse
-    // rows sorted by the fine internal row of their first R column, and per
-    // granule of 4 fine rows the first index into rr_crows (rr_ngran + 1).
-    int* rr_crows = nullptr;
-    int* rr_gptr = nullptr;
-    int rr_ngran = 0;
     int* gsf_rows = nullptr;
     int* gsr_rows = nullptr;
     std::vector<int> gsf_ptr, gsr_ptr;
@@ -188,9 +172,6 @@ struct decmg_gpu_ctx {
     double* seq_buf = nullptr;  // exact parallel projection chain scratch (seqsum.cuh), on first use
     int* seq_fallbacks = nullptr;  // device counter of segments that ran the literal chain
     int proj_seq = 0;           // literal single-lane projection chain instead (env DECMG_PROJ_SEQ=1)
-    int pair = 0;               // wavefront sweep pairs (pair.cu), opt-in: env DECMG_PAIR=1 (slower)
-    int pair_ch = 1;            // tiles per chunk (env DECMG_PAIR_CH)
-    int pair_lag = 1;           // sweep-2 lag in steps (env DECMG_PAIR_LAG)
     cudaStream_t io_stream = nullptr;        // chunked host copies (stage_rhs)
     // solve_batches (cycle.cu): second input/output buffers, staging and copy-out streams
     double* bproj2 = nullptr;
@@ -221,11 +202,8 @@ struct decmg_gpu_ctx {
     int rpt = 4;                // right-hand sides per thread in the vector mapping (env DECMG_RPT)
     double wtot0 = 0.0;         // sum of level-0 dual areas in the reference order
     int num_sms = 148;
-    int sweep2 = 0;             // fused sweep pairs, opt-in (env DECMG_SWEEP2=1; slower on B200)
     int pf = 56;                // row-kernel prefetch distance in rows, 0 = off (env DECMG_PF)
     int pfl = 2;                // prefetch into L1 (1) or L2 (2) (env DECMG_PFL)
-    int fuse_rr = 0;            // residual recomputed inside the restriction, opt-in (env DECMG_FUSE_RR=1; slower)
-    int rr_window = 0;          // residual + restriction through a shared-memory window, opt-in (env DECMG_RR_WINDOW=1; slower)
     int kmode = 2;              // row kernels: 2 auto (default), 0 pipelined, 1 high-occupancy (env DECMG_KERNEL)
     decmg_gpu::Timing timing;
     std::string err;
@@ -259,13 +237,33 @@ Status launch(decmg_gpu_ctx* c, int cls, double bytes, F&& f) {
     return cuda_status(cudaGetLastError(), "kernel launch");
 }
 
+// One-time setup per (device, kernel): cudaFuncSetAttribute applies to the
+// device current at the call, so a process with contexts on several devices
+// must repeat it for each. first_on_device(c, fn) is true on the first call
+// for (c->device, fn); block_occupancy caches the resident blocks per SM of
+// (device, fn) at the given block shape.
+inline bool first_on_device(const decmg_gpu_ctx* c, const void* fn) {
+    static std::mutex mu;
+    static std::set<std::pair<int, const void*>> seen;
+    std::lock_guard<std::mutex> g(mu);
+    return seen.emplace(c->device, fn).second;
+}
+inline int block_occupancy(const decmg_gpu_ctx* c, const void* fn, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, int, size_t>, int> cache;
+    std::lock_guard<std::mutex> g(mu);
+    const auto key = std::make_tuple(c->device, fn, threads, smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem) != cudaSuccess) nb = 0;
+    cache[key] = nb;
+    return nb;
+}
+
 inline unsigned grid_for(int64_t threads, int block) {
     return static_cast<unsigned>((threads + block - 1) / block);
 }
-
-// pair.cu: two Jacobi sweeps in one wavefront pass (x -> x'' in place, x' in x[cur ^ 1])
-Status pair_sweeps(decmg_gpu_ctx* c, int k, int key, int nrhs, double omega, const double* b, double* partial,
-                   int* grid, double bytes, int cls);
 
 // setup.cu
 Status build_from_base(decmg_gpu_ctx* c, const double* pos, int nv, const int* corners, int nt,

@@ -26,6 +26,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <cmath>
 #include <functional>
 
@@ -40,7 +41,9 @@ Status make_plan(const decmg_gpu_ctx* c, const decmg_gpu_plan* p, Plan* out) {
     if (p && p->smoother != DECMG_SMOOTHER_JACOBI && p->smoother != DECMG_SMOOTHER_GS &&
         p->smoother != DECMG_SMOOTHER_SGS && p->smoother != DECMG_SMOOTHER_CG)
         return Status::Err(DECMG_INVALID_ARGUMENT, "smoother: unknown smoother");
-    q.smoother = p ? p->smoother : DECMG_SMOOTHER_JACOBI;
+    // plan == NULL: standard_plan(levels, CycleKind::V) with its defaults
+    // (multigrid.hpp:88-89: pre = post = 3, SmootherConfig{} = Gauss-Seidel)
+    q.smoother = p ? p->smoother : DECMG_SMOOTHER_GS;
     q.omega = p ? p->jacobi_omega : 2.0 / 3.0;
     if (p && p->walk) {
         q.walk = p->walk;
@@ -49,8 +52,8 @@ Status make_plan(const decmg_gpu_ctx* c, const decmg_gpu_plan* p, Plan* out) {
         for (int i = 0; i < L - 1; ++i) q.walk.push_back('u');
     }
     for (int k = 0; k < L; ++k) {
-        q.pre.push_back(p ? (p->pre ? p->pre[k] : p->pre_all) : 2);
-        q.post.push_back(p ? (p->post ? p->post[k] : p->post_all) : 2);
+        q.pre.push_back(p ? (p->pre ? p->pre[k] : p->pre_all) : 3);
+        q.post.push_back(p ? (p->post ? p->post[k] : p->post_all) : 3);
     }
     // CyclePlan::validate (multigrid.cpp:131-143)
     int level = 0;
@@ -160,12 +163,9 @@ Status project_chain_seq(decmg_gpu_ctx* c, int nrhs, const double* d_b, int r0, 
     const Level& L = c->lv[0];
     double* state = c->dsmall + 160;
     const size_t smem = static_cast<size_t>(kProjStages) * proj_rows(nrhs) * nrhs * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    if (first_on_device(c, reinterpret_cast<const void*>(k_project_sums)))
         DG_CUDA(cudaFuncSetAttribute(k_project_sums, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kProjStages * kProjTileBytes));
-        attr = true;
-    }
     double* prod = c->r;  // scratch [n0][max_nrhs]: the residual buffer is free outside a cycle
     const int64_t t = static_cast<int64_t>(r1 - r0) * nrhs;
     DG_TRY(launch(c, kNorms, 8.0 * (r1 - r0) + 16.0 * t, [&] {
@@ -251,10 +251,14 @@ Status stage_rhs(decmg_gpu_ctx* c, int nrhs, const double* h_b, bool project, do
 // iterates and histories are the same bits. The body is captured from
 // Driver::one_cycle itself: the fused-norm hook adds the check kernels and
 // the IF node to the capture and redirects the rest of the cycle into the IF
-// body. Cycles preserve each level's ping-pong parity, so one captured cycle
-// is valid for every iteration; the key includes that parity.
+// body. One captured cycle is valid for every iteration only if the cycle
+// preserves level 0's ping-pong parity (coarser levels restart from zero on
+// every descent); a cycle that flips it (an odd number of level-0 Jacobi
+// sweeps, e.g. V(2,1)) is detected after the capture and *graphed stays false,
+// so solve() runs the host loop. The key includes every level's parity.
 Status solve_graph(decmg_gpu_ctx* c, Driver& dr, const Plan& plan, int nrhs, unsigned all, double tol,
-                   int max_cycles, double* denom, double* dres, int64_t total) {
+                   int max_cycles, double* denom, double* dres, int64_t total, bool* graphed) {
+    *graphed = false;
     if (!c->gstate_raw) DG_TRY(dalloc(c, &c->gstate_raw, (sizeof(SolveState) + 7) / 8));
     SolveState* gst = reinterpret_cast<SolveState*>(c->gstate_raw);
     if (max_cycles > c->hist_cap) {
@@ -264,10 +268,13 @@ Status solve_graph(decmg_gpu_ctx* c, Driver& dr, const Plan& plan, int nrhs, uns
         DG_CUDA(cudaMalloc(&c->hist_dev, sizeof(double) * max_cycles * 32));
         c->hist_cap = max_cycles;
     }
-    std::string key = plan.walk + "|" + std::to_string(plan.smoother) + "|" + std::to_string(plan.omega) + "|" +
+    // omega by its exact bits: two omegas that print alike must not share a graph
+    uint64_t omega_bits = 0;
+    std::memcpy(&omega_bits, &plan.omega, sizeof omega_bits);
+    std::string key = plan.walk + "|" + std::to_string(plan.smoother) + "|" + std::to_string(omega_bits) + "|" +
                       std::to_string(nrhs) + "|" + std::to_string(reinterpret_cast<uintptr_t>(dr.b0)) + "|" +
                       std::to_string(reinterpret_cast<uintptr_t>(c->hist_dev)) + "|" +
-                      std::to_string(reinterpret_cast<uintptr_t>(c->red)) + "|" + std::to_string(c->pair) + "|";
+                      std::to_string(reinterpret_cast<uintptr_t>(c->red)) + "|";
     for (size_t k = 0; k < c->lv.size(); ++k)
         key += std::to_string(plan.pre[k]) + "," + std::to_string(plan.post[k]) + "," +
                std::to_string(c->lv[k].cur) + std::to_string(c->lv[k].x_zero ? 1 : 0) + ";";
@@ -325,6 +332,12 @@ Status solve_graph(decmg_gpu_ctx* c, Driver& dr, const Plan& plan, int nrhs, uns
             split = true;
             return Status::Ok();
         };
+        // host view of the ping-pong state before the captured cycle: the graph
+        // replays one cycle with fixed buffer pointers, which is valid only if
+        // the cycle leaves level 0's parity unchanged (an even number of level-0
+        // Jacobi sweeps; coarser levels restart from zero on every descent)
+        std::vector<std::pair<int, bool>> st0;
+        for (const Level& L : c->lv) st0.emplace_back(L.cur, L.x_zero);
         hs = dr.one_cycle(plan);
         dr.fuse_hook = nullptr;
         dr.fuse_hist = nullptr;
@@ -341,12 +354,23 @@ Status solve_graph(decmg_gpu_ctx* c, Driver& dr, const Plan& plan, int nrhs, uns
             cudaGraphDestroy(g);
             return hs;
         }
+        if (c->lv[0].cur != st0[0].first) {
+            // parity-changing cycle (e.g. V(2,1) Jacobi): nothing was executed,
+            // so restore the host state and let the caller run the host loop
+            cudaGraphDestroy(g);
+            for (size_t k = 0; k < c->lv.size(); ++k) {
+                c->lv[k].cur = st0[k].first;
+                c->lv[k].x_zero = st0[k].second;
+            }
+            return Status::Ok();
+        }
         DG_CUDA(cudaGraphInstantiate(&exec, g, 0));
         c->graphs.push_back({key, g, exec});
     }
     DG_TRY(launch(c, kNorms, 0.0, [&] { k_solve_init<<<1, 1, 0, c->stream>>>(gst, 1, all, max_cycles, tol); }));
     DG_CUDA(cudaGraphLaunch(exec, c->stream));
     ++c->launch_count;
+    *graphed = true;
     return Status::Ok();
 }
 
@@ -422,8 +446,10 @@ Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, co
     if (c->graph && !c->timing.enabled && max_cycles >= 2 && c->lv.size() > 1) {
         DG_TRY(dr.one_cycle(plan));  // cycle 0 (from x0; its first sweep carries no residual)
         cyc = 1;
-        if (dr.can_fuse(plan)) {  // cycles 1.. on the device
-            DG_TRY(solve_graph(c, dr, plan, nrhs, all, tol, max_cycles, denom, dres, total));
+        bool on_device = false;
+        if (dr.can_fuse(plan))  // cycles 1.. on the device
+            DG_TRY(solve_graph(c, dr, plan, nrhs, all, tol, max_cycles, denom, dres, total, &on_device));
+        if (on_device) {
             SolveState st;
             std::vector<double> hist(static_cast<size_t>(max_cycles) * nrhs);
             DG_CUDA(cudaMemcpyAsync(&st, c->gstate_raw, sizeof(SolveState), cudaMemcpyDeviceToHost, c->stream));

@@ -44,53 +44,42 @@ struct Driver {
 
     // Launch the pipelined persistent row kernel on an ELL operator.
     // Returns the grid size in *grid (the number of norm partials for OP_RES_NORM).
-    template <int OP, int W, int W2 = 0>
+    template <int OP, int W>
     Status pipe(int cls, double bytes, int nrows, const int* eci, const double* ev, const int* erow,
                 const double* x, const double* b, double* out, double* partial, const int* zr, double omega,
-                int* grid = nullptr, const PipeArgs* fine = nullptr) {
+                int* grid = nullptr) {
         Status st;
         DISPATCH_BP(key, {
             PipeArgs a{0, nrhs, eci, ev, erow, x, b, out, partial, zr, omega, nrows, c->pf, c->pfl};
-            if (fine) {  // OP_RESTRICT_RES: the fine level's L and right-hand side
-                a.fci = fine->fci;
-                a.fv = fine->fv;
-                a.fb = fine->fb;
-                a.n = fine->n;
-            }
             // pipelined kernel for the 7/8-wide operators (L, R), the
             // high-occupancy kernel for P (2-wide rows); env DECMG_KERNEL forces one
-            const bool ell = OP != OP_RESTRICT_RES && (c->kmode == 1 || (c->kmode == 2 && W == 2));
+            const bool ell = c->kmode == 1 || (c->kmode == 2 && W == 2);
             if (ell) {
                 const unsigned g = grid_for(static_cast<int64_t>(nrows) * (BP / RPT), kBlock);
-                static bool carved = false;
-                if (!carved && c->carveout >= 0) {
+                if (c->carveout >= 0 && first_on_device(c, reinterpret_cast<const void*>(k_rowop_ell<BP, RPT, W, OP>)))
                     cudaFuncSetAttribute(k_rowop_ell<BP, RPT, W, OP>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          c->carveout);
-                    carved = true;
-                }
                 st = launch(c, cls, bytes, [&] { k_rowop_ell<BP, RPT, W, OP><<<g, kBlock, 0, c->stream>>>(a, nrows); });
                 if (grid) *grid = static_cast<int>(g);
             } else {  // persistent pipelined kernel with the TMA-bulk index ring
                 using G = PipeGeom<BP, RPT, W>;
                 static_assert((G::ROWS * 4 % 16 == 0 && G::CI_BYTES % 16 == 0) || BP / RPT > 8, "pipe tile");
                 const int ntiles = (nrows + G::ROWS - 1) / G::ROWS;
-                const int per_sm = OP == OP_RESTRICT_RES ? 2 : kPipeCtasPerSm;
+                const int per_sm = kPipeCtasPerSm;
                 const int g = ntiles < per_sm * c->num_sms ? ntiles : per_sm * c->num_sms;
-                static bool attr = false;
-                if (!attr) {
-                    cudaFuncSetAttribute(k_rowop_pipe<BP, RPT, W, OP, W2>,
+                if (first_on_device(c, reinterpret_cast<const void*>(k_rowop_pipe<BP, RPT, W, OP>))) {
+                    cudaFuncSetAttribute(k_rowop_pipe<BP, RPT, W, OP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(G::PSMEM));
                     // the common carve-out only where all per_sm CTAs still fit in it (the
                     // single-RHS tiles need ~80 KB each: the driver's choice keeps them resident)
                     if (c->carveout >= 0 &&
                         per_sm * (G::PSMEM + 1024.0) <= c->carveout / 100.0 * kSmemPerSm)
-                        cudaFuncSetAttribute(k_rowop_pipe<BP, RPT, W, OP, W2>,
+                        cudaFuncSetAttribute(k_rowop_pipe<BP, RPT, W, OP>,
                                              cudaFuncAttributePreferredSharedMemoryCarveout, c->carveout);
-                    attr = true;
                 }
                 a.ntiles = ntiles;
                 st = launch(c, cls, bytes, [&] {
-                    k_rowop_pipe<BP, RPT, W, OP, W2><<<g, kPipeThreads, G::PSMEM, c->stream>>>(a);
+                    k_rowop_pipe<BP, RPT, W, OP><<<g, kPipeThreads, G::PSMEM, c->stream>>>(a);
                 });
                 if (grid) *grid = g;
             }
@@ -109,47 +98,6 @@ struct Driver {
             DG_CUDA(cudaMemsetAsync(xcur(L), 0, sizeof(double) * L.nv * nrhs, c->stream));
             L.x_zero = false;
         }
-        return Status::Ok();
-    }
-
-    // Fused sweep pair on level k (k_sweep2); norm_out != nullptr: also the
-    // residual norm of the incoming x (level 0, fused cycle-residual).
-    Status sweep_pair(int k, const Plan& plan, double* norm_out) {
-        Level& L = c->lv[k];
-        const bool zero = L.x_zero;
-        const double R = nrhs;
-        const double bytes = zero ? 8.0 * L.nv + 12.0 * L.nnzL + 4.0 * L.nv + 16.0 * L.nv * R
-                                  : 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
-        const int ntiles = (L.nv + kS2Rows - 1) / kS2Rows;
-        const size_t smem = static_cast<size_t>(kS2Rows + L.S2_maxhalo) * nrhs * sizeof(double);
-        S2Args a{L.nv, nrhs, L.Le_ci, L.Le_v, L.Le_row, L.S2_slot, L.S2_hptr, L.S2_halo, L.diag_i, xcur(L), bptr(k),
-                 L.x[L.cur ^ 1], c->red, plan.omega};
-        const int cls = zero ? kZeroSweep : (k == 0 ? kFineSweep : kCoarseLevels);
-        Status st;
-        DISPATCH_BP(key, {
-            auto go = [&](void (*kern)(S2Args)) {
-                // opt in to > 48 KB of dynamic shared memory, once per kernel
-                static std::vector<const void*> done;
-                if (std::find(done.begin(), done.end(), reinterpret_cast<const void*>(kern)) == done.end()) {
-                    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-                    done.push_back(reinterpret_cast<const void*>(kern));
-                }
-                st = launch(c, cls, bytes, [&] { kern<<<ntiles, kBlock, smem, c->stream>>>(a); });
-            };
-            if (L.Le_w == 7) {
-                if (zero) go(k_sweep2<BP, RPT, 7, true, false>);
-                else if (norm_out) go(k_sweep2<BP, RPT, 7, false, true>);
-                else go(k_sweep2<BP, RPT, 7, false, false>);
-            } else {
-                if (zero) go(k_sweep2<BP, RPT, 8, true, false>);
-                else if (norm_out) go(k_sweep2<BP, RPT, 8, false, true>);
-                else go(k_sweep2<BP, RPT, 8, false, false>);
-            }
-        })
-        DG_TRY(st);
-        if (norm_out) DG_TRY(reduce_partials(ntiles, norm_out, 2, fuse_denom));
-        L.cur ^= 1;
-        L.x_zero = false;
         return Status::Ok();
     }
 
@@ -284,47 +232,15 @@ struct Driver {
         const double R = nrhs;
         for (int it = 0; it < iters;) {
             const bool fuse_norm = k == 0 && it == 0 && fuse_hist && !L.x_zero;
-            if (iters - it >= 2 && c->pair && !L.x_zero && L.Le_ci && tpr <= 8 && !(fuse_norm && fuse_hook)) {
-                // two sweeps in one wavefront pass (pair.cu); x'' lands in x[cur]
-                const double bytes = 2.0 * (12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R);
-                int g = 0;
-                DG_TRY(pair_sweeps(c, k, key, nrhs, plan.omega, bptr(k), fuse_norm ? c->red : nullptr, &g, bytes,
-                                   k == 0 ? kFineSweep : kCoarseLevels));
-                if (fuse_norm) {
-                    DG_TRY(reduce_partials(g, fuse_hist, 2, fuse_denom));
-                    fuse_hist = nullptr;
-                }
-                it += 2;
-                continue;
-            }
-            if (iters - it >= 2 && L.S2_maxhalo >= 0 && tpr <= 8 && c->sweep2) {
-                DG_TRY(sweep_pair(k, plan, fuse_norm ? fuse_hist : nullptr));
-                it += 2;
-                if (fuse_norm) {
-                    fuse_hist = nullptr;
-                    if (fuse_hook) {
-                        bool stop = false;
-                        DG_TRY(fuse_hook(L.x[L.cur ^ 1], &stop));
-                        if (stop) {
-                            L.cur ^= 1;  // x_prev stays the current iterate
-                            stopped = true;
-                            return Status::Ok();
-                        }
-                    }
-                }
-                continue;
-            }
             double* xo = L.x[L.cur ^ 1];
             const double* b = bptr(k);
             if (L.x_zero) {
                 const double bytes = 8.0 * L.nv + 16.0 * L.nv * R;
                 if (c->carveout >= 0) {
                     DISPATCH_BP(key, {
-                        static bool carved = false;  // per (BP, RPT)
-                        if (!carved)
+                        if (first_on_device(c, reinterpret_cast<const void*>(k_sweep_zero<BP, RPT>)))
                             cudaFuncSetAttribute(k_sweep_zero<BP, RPT>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                                  c->carveout);
-                        carved = true;
                     })
                 }
                 DG_TRY(launch(c, kZeroSweep, bytes, [&] {
@@ -378,58 +294,6 @@ struct Driver {
         const double R = nrhs;
         const double* x = xcur(L);
         const double* b = bptr(k);
-        if (c->rr_window && L.rr_crows && tpr <= 8 && !c->fuse_rr) {
-            // residual kept in a shared-memory window, restriction in the same pass
-            const double bytes = 12.0 * L.nnzR + 4.0 * (C.nv + 1) + 12.0 * L.nnzL + 4.0 * (L.nv + 1) +
-                                 16.0 * L.nv * R + 8.0 * C.nv * R;
-            const int cls = k == 0 ? kRestrict : kCoarseLevels;
-            const int* zr = c->dirichlet ? C.bd_i : nullptr;
-            Status st;
-            DISPATCH_BP(key, {
-                auto go = [&](auto wl, auto wr) {
-                    constexpr int WL = decltype(wl)::value, WRr = decltype(wr)::value;
-                    using G = PipeGeom<BP, RPT, WL>;
-                    auto kern = k_res_restrict<BP, RPT, WL, WRr>;
-                    const size_t smem = static_cast<size_t>(kPipeStages) * G::STAGE_BYTES +
-                                        static_cast<size_t>(kRRWindow) * G::ROWS * BP * sizeof(double);
-                    static bool attr = false;
-                    if (!attr) {
-                        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-                        attr = true;
-                    }
-                    const int ntiles = (L.nv + G::ROWS - 1) / G::ROWS;
-                    const int g = ntiles < 2 * c->num_sms ? ntiles : 2 * c->num_sms;
-                    RRArgs a{ntiles, nrhs, L.nv, L.Le_ci, L.Le_v, L.Le_row, x, b, L.Re_ci, L.Re_v, L.rr_crows,
-                             L.rr_gptr, L.rr_ngran, C.b, zr, c->pf};
-                    return launch(c, cls, bytes, [&] { kern<<<g, kPipeThreads, smem, c->stream>>>(a); });
-                };
-                using I7 = std::integral_constant<int, 7>;
-                using I8 = std::integral_constant<int, 8>;
-                if (L.Le_w == 7) st = L.Re_w == 7 ? go(I7{}, I7{}) : go(I7{}, I8{});
-                else st = L.Re_w == 7 ? go(I8{}, I7{}) : go(I8{}, I8{});
-            })
-            return st;
-        }
-        if (c->fuse_rr && L.Le_ci && L.Re_ci && tpr <= 8) {
-            // one pass: every R row recomputes the fine residuals it needs
-            const double bytes = 12.0 * L.nnzR + 4.0 * (C.nv + 1) + 12.0 * L.nnzL + 4.0 * (L.nv + 1) +
-                                 16.0 * L.nv * R + 8.0 * C.nv * R;
-            PipeArgs fine{};
-            fine.fci = L.Le_ci;
-            fine.fv = L.Le_v;
-            fine.fb = b;
-            fine.n = L.nv;
-            const int* zr = c->dirichlet ? C.bd_i : nullptr;
-            const int cls = k == 0 ? kRestrict : kCoarseLevels;
-            auto go = [&](auto wr, auto wl) {
-                return pipe<OP_RESTRICT_RES, decltype(wr)::value, decltype(wl)::value>(
-                    cls, bytes, C.nv, L.Re_ci, L.Re_v, L.Re_row, x, nullptr, C.b, nullptr, zr, 0.0, nullptr, &fine);
-            };
-            using I7 = std::integral_constant<int, 7>;
-            using I8 = std::integral_constant<int, 8>;
-            if (L.Re_w == 7) return L.Le_w == 7 ? go(I7{}, I7{}) : go(I7{}, I8{});
-            return L.Le_w == 7 ? go(I8{}, I7{}) : go(I8{}, I8{});
-        }
         const double rbytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
         if (L.Le_ci && tpr <= 8) {
             DG_TRY(PIPE_W(L.Le_w, OP_RES_STORE, k == 0 ? kFineResidual : kCoarseLevels, rbytes, L.nv, L.Le_ci,
@@ -501,7 +365,7 @@ struct Driver {
         const int Lc = static_cast<int>(c->lv.size());
         const int m = Lc - 1 - level;
         if (!c->vtail || level < 1 || m < 1 || m >= kTailMax || tpr > 8 || fuse_hist) return false;
-        if (plan.smoother != DECMG_SMOOTHER_JACOBI || c->pair) return false;
+        if (plan.smoother != DECMG_SMOOTHER_JACOBI) return false;
         if (static_cast<int64_t>(c->lv[level].nv) * nrhs > c->vtail_items) return false;
         if (w + 2 * m > static_cast<int>(plan.walk.size())) return false;
         for (int i = 0; i < m; ++i)
@@ -558,12 +422,7 @@ struct Driver {
         Status st;
         DISPATCH_BP(key, {
             auto kern = k_vtail<BP, RPT>;
-            static int blocks = -1;
-            if (blocks < 0) {
-                int nb = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kBlock, 0);
-                blocks = nb >= 1 ? c->num_sms : 0;
-            }
+            const int blocks = block_occupancy(c, reinterpret_cast<const void*>(kern), kBlock, 0) >= 1 ? c->num_sms : 0;
             if (blocks == 0) {
                 st = Status::Err(DECMG_CUDA, "bottom-of-V kernel does not fit on an SM");
             } else {

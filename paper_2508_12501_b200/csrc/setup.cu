@@ -24,7 +24,6 @@ namespace decmg_gpu {
 namespace {
 
 constexpr int kBlock = 256;
-constexpr int kS2RowsHost = 128;  // == kS2Rows (rowkernels.cuh)
 
 // ---------------------------------------------------------------- Vec3 -----
 // proj/include/decmg/geometry.hpp:12-43, component formulas verbatim.
@@ -713,19 +712,6 @@ __global__ void k_gs_keys(int n, const int* __restrict__ ord, const int* __restr
     q[r] = static_cast<int>(r);
 }
 
-// Coarse rows by the 4-row granule of their first (renumbered) R column.
-__global__ void k_rr_count(int nc, const int* __restrict__ rp, const int* __restrict__ ci, int* __restrict__ cnt) {
-    const int64_t q = gtid();
-    if (q < nc) atomicAdd(&cnt[ci[rp[q]] / 4], 1);
-}
-__global__ void k_rr_fill(int nc, const int* __restrict__ rp, const int* __restrict__ ci,
-                          const int* __restrict__ gptr, int* __restrict__ cursor, int* __restrict__ crows) {
-    const int64_t q = gtid();
-    if (q >= nc) return;
-    const int g = ci[rp[q]] / 4;
-    crows[gptr[g] + atomicAdd(&cursor[g], 1)] = static_cast<int>(q);
-}
-
 __global__ void k_invert(int n, const int* __restrict__ ord, int* __restrict__ inv) {
     const int64_t q = gtid();
     if (q < n) inv[ord[q]] = static_cast<int>(q);
@@ -1093,60 +1079,6 @@ Status build_gs_schedule(decmg_gpu_ctx* c, Level& m) {
     return Status::Ok();
 }
 
-// Tiles and halos for the fused sweep pairs (rowkernels.cuh k_sweep2).
-Status build_sweep2(decmg_gpu_ctx* c, Level& m) {
-    if (!m.Le_ci || !m.Le_row) return Status::Ok();
-    const int n = m.nv, W = m.Le_w, TR = kS2RowsHost;
-    const int npad = (n + 223) / 224 * 224;
-    std::vector<int> ci(static_cast<size_t>(npad) * W), rowid(npad);
-    DG_CUDA(cudaMemcpy(ci.data(), m.Le_ci, sizeof(int) * ci.size(), cudaMemcpyDeviceToHost));
-    DG_CUDA(cudaMemcpy(rowid.data(), m.Le_row, sizeof(int) * npad, cudaMemcpyDeviceToHost));
-    std::vector<int> pos_of(n, -1);
-    for (int q = 0; q < n; ++q) pos_of[rowid[q] & ((1 << kRowBits) - 1)] = q;
-    const int ntiles = (n + TR - 1) / TR;
-    std::vector<int> hptr(ntiles + 1, 0), halo, slot(static_cast<size_t>(npad) * W, -1);
-    std::vector<int> stamp(n, -1), hslot(n, -1);
-    int maxh = 0;
-    for (int t = 0; t < ntiles; ++t) {
-        const int t0 = t * TR, t1 = std::min(n, t0 + TR);
-        int nh = 0;
-        for (int q = t0; q < t1; ++q)
-            for (int j = 0; j < W; ++j) {
-                const int v = ci[static_cast<size_t>(q) * W + j];
-                if (v < 0) continue;
-                const int qq = pos_of[v];
-                int sl;
-                if (qq >= t0 && qq < t1) {
-                    sl = qq - t0;
-                } else {
-                    if (stamp[qq] != t) {
-                        stamp[qq] = t;
-                        hslot[qq] = TR + nh++;
-                        halo.push_back(qq);
-                    }
-                    sl = hslot[qq];
-                }
-                slot[static_cast<size_t>(q) * W + j] = sl;
-            }
-        hptr[t + 1] = hptr[t] + nh;
-        maxh = std::max(maxh, nh);
-    }
-    DG_TRY(dalloc(c, &m.S2_hptr, hptr.size()));
-    DG_TRY(dalloc(c, &m.S2_halo, halo.size()));
-    DG_TRY(dalloc(c, &m.S2_slot, slot.size()));
-    DG_CUDA(cudaMemcpy(m.S2_hptr, hptr.data(), sizeof(int) * hptr.size(), cudaMemcpyHostToDevice));
-    if (!halo.empty())
-        DG_CUDA(cudaMemcpy(m.S2_halo, halo.data(), sizeof(int) * halo.size(), cudaMemcpyHostToDevice));
-    DG_CUDA(cudaMemcpy(m.S2_slot, slot.data(), sizeof(int) * slot.size(), cudaMemcpyHostToDevice));
-    m.S2_maxhalo = maxh;
-    // the fused pair keeps (tile + halo) rows x nrhs doubles in shared memory
-    if (static_cast<size_t>(TR + maxh) * c->max_nrhs * sizeof(double) > 200 * 1024) m.S2_maxhalo = -1;
-    if (std::getenv("DECMG_DEBUG"))
-        std::fprintf(stderr, "decmg: level nv=%d sweep-pair tiles=%d halo avg=%.1f max=%d%s\n", n, ntiles,
-                     static_cast<double>(halo.size()) / ntiles, maxh, m.S2_maxhalo < 0 ? " (disabled)" : "");
-    return Status::Ok();
-}
-
 // Internal numbering for every level except the coarsest (its CG runs
 // sequentially in the reference order): Morton order, the renumbered L, P, R
 // (common.cuh Level), their ELL copies, diag and boundary flags by internal row.
@@ -1192,23 +1124,7 @@ Status build_orders(decmg_gpu_ctx* c) {
         DG_TRY(build_ell(c, m.nv, m.Po_rp, m.Po_ci, m.Po_v, nullptr, 2, false, &m.Pe_ci, &m.Pe_v, nullptr));
         DG_TRY(build_ell(c, cm.nv, m.Ro_rp, m.Ro_ci, m.Ro_v, nullptr, -8, false, &m.Re_ci, &m.Re_v, &m.Re_row,
                          &m.Re_w));
-        DG_TRY(build_sweep2(c, m));
         DG_TRY(build_gs_schedule(c, m));
-        if (m.Le_ci && m.Re_ci) {  // fused residual + restriction lookup
-            TmpPool tp(c->stream);
-            const int ng = (m.nv + 3) / 4;
-            int *cnt, *cursor;
-            DG_TRY(tp.get(&cnt, ng + 1));
-            DG_TRY(tp.get(&cursor, ng + 1));
-            DG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * (ng + 1), c->stream));
-            DG_CUDA(cudaMemsetAsync(cursor, 0, sizeof(int) * (ng + 1), c->stream));
-            LAUNCH(4, cm.nv, k_rr_count, cm.nv, m.Ro_rp, m.Ro_ci, cnt);
-            DG_TRY(dalloc(c, &m.rr_gptr, ng + 1));
-            DG_TRY(exclusive_scan(c, cnt, m.rr_gptr, ng));
-            DG_TRY(dalloc(c, &m.rr_crows, cm.nv));
-            LAUNCH(4, cm.nv, k_rr_fill, cm.nv, m.Ro_rp, m.Ro_ci, m.rr_gptr, cursor, m.rr_crows);
-            m.rr_ngran = ng;
-        }
         if (m.Pe_ci && !m.Le_row) {  // P rows share L's row ids
             m.Pe_ci = nullptr;
             m.Pe_v = nullptr;

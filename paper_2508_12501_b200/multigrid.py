@@ -36,13 +36,13 @@ class Smoother(enum.Enum):
 
 @dataclass
 class SmootherConfig:
-    # The reference default is GaussSeidel (multigrid.hpp:58), a sequential
-    # sweep. The device implements weighted Jacobi (multigrid.cpp:36-56) and
-    # the forward / symmetric Gauss-Seidel sweeps (multigrid.cpp:13-34) as a
-    # level schedule that is bit-identical to the sequential sweep (DESIGN.md
-    # "Gauss-Seidel"); the default stays Jacobi (BASELINE north star). Cg =
-    # cg_fixed (multigrid.cpp:63-91) with tree dots (within rounding).
-    method: Smoother = Smoother.WeightedJacobi
+    # Default = the reference's GaussSeidel (multigrid.hpp:58): the forward
+    # lexicographic sweep (multigrid.cpp:13-34), run on the device as a level
+    # schedule bit-identical to the sequential sweep.
+    # WeightedJacobi (multigrid.cpp:36-56) is the BASELINE configs' smoother and
+    # is selected explicitly there. Cg = cg_fixed (multigrid.cpp:63-91) with
+    # tree dots (within rounding).
+    method: Smoother = Smoother.GaussSeidel
     jacobi_omega: float = 2.0 / 3.0
 
 

@@ -87,17 +87,17 @@ def test_ico_faces_outward():
 
 def test_standard_plans_match_reference_walks():
     w = lambda s: [d.Transition.Down if ch == "d" else d.Transition.Up for ch in s]
-    assert d.standard_plan(2, d.CycleKind.V).walk == w("du")
-    assert d.standard_plan(3, d.CycleKind.V).walk == w("dduu")
-    assert d.standard_plan(3, d.CycleKind.W).walk == w("dduduu")
-    assert d.standard_plan(3, d.CycleKind.F).walk == w("dduduu")
+    assert d.standard_plan(2, d.CycleKind.V, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi)).walk == w("du")
+    assert d.standard_plan(3, d.CycleKind.V, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi)).walk == w("dduu")
+    assert d.standard_plan(3, d.CycleKind.W, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi)).walk == w("dduduu")
+    assert d.standard_plan(3, d.CycleKind.F, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi)).walk == w("dduduu")
     for levels in range(1, 6):
         for kind in d.CycleKind:
-            p = d.standard_plan(levels, kind)
+            p = d.standard_plan(levels, kind, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
             p.validate(levels)
             if levels > 1:
                 assert p.depth() == levels
-    w4 = d.standard_plan(4, d.CycleKind.W)
+    w4 = d.standard_plan(4, d.CycleKind.W, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     level, visits = 0, 0
     for t in w4.walk:
         level += 1 if t == d.Transition.Down else -1

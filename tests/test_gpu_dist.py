@@ -24,7 +24,7 @@ def test_partitioned_run_cycle_bitwise(world):
     dh = d.DistributedHierarchy(base, nsub, world, agglomerate_below=200)
     assert dh.agglomeration_level >= 2  # several distributed levels
     assert dh.halo0 > 0
-    plan = d.standard_plan(dh.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(dh.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     plan.cycles = 5
     res = dh.run_cycle(plan, b)
     ox, oh = o.run_cycles(b, ncycles=5)
@@ -37,9 +37,9 @@ def test_partitioned_gmg_solve_matches_single_gpu(world):
     base, nsub = "ico", 7
     h = d.MultigridHierarchy.from_base(base, nsub)
     b = h.make_rhs("ylm", 1)
-    rep1 = d.gmg_solve(h, d.standard_plan(h.levels(), d.CycleKind.V, 2, 2), b, 1e-8, 200)
+    rep1 = d.gmg_solve(h, d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi)), b, 1e-8, 200)
     dh = d.DistributedHierarchy(base, nsub, world, agglomerate_below=500)
-    rep = dh.gmg_solve(d.standard_plan(dh.levels(), d.CycleKind.V, 2, 2), b, 1e-8, 200)
+    rep = dh.gmg_solve(d.standard_plan(dh.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi)), b, 1e-8, 200)
     assert rep.iterations == rep1.iterations
     np.testing.assert_array_equal(rep.solution, rep1.solution)
     np.testing.assert_allclose(rep.residual_history, rep1.residual_history, rtol=RTOL)
@@ -50,7 +50,7 @@ def test_partitioned_dirichlet_and_batch():
     o = OracleHierarchy("square", 7, True)
     b = o.rhs("sinsin", 0)
     dh = d.DistributedHierarchy("square", 7, 4, dirichlet=True, agglomerate_below=100)
-    plan = d.standard_plan(dh.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(dh.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     plan.cycles = 4
     res = dh.run_cycle(plan, b)
     ox, oh = o.run_cycles(b, ncycles=4)
@@ -59,7 +59,7 @@ def test_partitioned_dirichlet_and_batch():
     nrhs = 16
     h = d.MultigridHierarchy.from_base("ico", 6, max_nrhs=nrhs)
     B = h.project_compatible(h.make_rhs("uniform", 9, nrhs))
-    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     plan.cycles = 3
     r1 = h.run_cycle(plan, B)
     dh = d.DistributedHierarchy("ico", 6, 4, max_nrhs=nrhs, agglomerate_below=300)
@@ -75,6 +75,6 @@ def test_nccl_single_rank_world():
     dh = d.DistributedHierarchy("ico", 5, 1, rank=0, nccl_id=uid)
     h = d.MultigridHierarchy.from_base("ico", 5)
     b = h.project_compatible(h.make_rhs("uniform", 2))
-    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     plan.cycles = 3
     np.testing.assert_array_equal(dh.run_cycle(plan, b).x, h.run_cycle(plan, b).x)

@@ -153,14 +153,14 @@ def test_batched_rhs_match_single_rhs_oracle():
     o = OracleHierarchy(base, nsub)
     B = h.make_rhs("uniform", 100, nrhs)
     Bp = np.stack([o.project(B[:, j]) for j in range(nrhs)], axis=1)
-    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     plan.cycles = 6
     res = h.run_cycle(plan, Bp, np.zeros_like(Bp))
     for j in range(nrhs):
         ox, oh = o.run_cycles(Bp[:, j], ncycles=6)
         np.testing.assert_array_equal(res.x[:, j], ox)
         assert np.all(np.abs(res.residual_history[:, j] - oh) <= RTOL_HIST * oh)
-    rep = d.gmg_solve(h, d.standard_plan(h.levels(), d.CycleKind.V, 2, 2), B, 1e-8, 100)
+    rep = d.gmg_solve(h, d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi)), B, 1e-8, 100)
     for j in range(nrhs):
         ox, oh, oit, _ = o.solve(B[:, j], tol=1e-8, max_cycles=100)
         assert abs(rep.iterations[j] - oit) <= 1
@@ -173,14 +173,14 @@ def test_w_and_f_walks_bitwise():
     o = OracleHierarchy("equi:4:8:1.0", 3)
     b = o.project(o.rhs("lr", 11))
     for kind in (d.CycleKind.W, d.CycleKind.F):
-        plan = d.standard_plan(h.levels(), kind, 2, 2)
+        plan = d.standard_plan(h.levels(), kind, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
         plan.cycles = 4
         res = h.run_cycle(plan, b)
         ox, oh = o.run_cycles(b, ncycles=4, walk=plan.walk_string())
         np.testing.assert_array_equal(res.x, ox)
         assert np.all(np.abs(res.residual_history - oh) <= RTOL_HIST * oh)
     # truncated walk that bottoms out above the coarsest level (multigrid.cpp:271-275)
-    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     plan.walk = [d.Transition.Down, d.Transition.Down, d.Transition.Up, d.Transition.Up]
     plan.cycles = 3
     res = h.run_cycle(plan, b)
@@ -201,7 +201,7 @@ def test_reference_unit_semantics():
     for k in range(4):
         lap = h.apply(k, "L", np.ones(h.n(k)))
         assert np.max(np.abs(lap)) <= 1e-12 * np.max(np.abs(h.export(k, "L_values")))
-    plan = d.standard_plan(4, d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(4, d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     plan.cycles = 3
     z = np.zeros(h.n())
     res = h.run_cycle(plan, z, z)
@@ -218,14 +218,14 @@ def test_reference_unit_semantics():
         np.testing.assert_array_equal(r, r2)
     one = d.MultigridHierarchy.from_base("equi:4:8:1.0", 0)
     b = one.project_compatible(one.make_rhs("lr", 5))
-    p1 = d.standard_plan(1, d.CycleKind.V)
+    p1 = d.standard_plan(1, d.CycleKind.V, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     r = one.run_cycle(p1, b, np.zeros_like(b)).residual_history
     assert r[-1] <= 1e-12
 
 
 def test_errors_surface_like_the_reference():
     h = d.MultigridHierarchy.from_base("square", 2)
-    plan = d.standard_plan(h.levels(), d.CycleKind.V)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     bad = d.CyclePlan(walk=[d.Transition.Down, d.Transition.Down, d.Transition.Up], pre=[1] * 3, post=[1] * 3)
     with pytest.raises(ValueError, match="does not return"):
         h.run_cycle(bad, np.zeros(h.n()))
@@ -239,6 +239,9 @@ def test_errors_surface_like_the_reference():
            dict(nv=1, L_row_ptr=[0, 1], L_col_idx=[0], L_values=[1.0], dual_areas=[1.0])]
     hz = d.MultigridHierarchy.from_levels(lv2)
     with pytest.raises(RuntimeError, match="jacobi: zero diagonal at row 1"):
+        hz.run_cycle(d.standard_plan(2, d.CycleKind.V, 1, 1, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi)), np.ones(2))
+    # the default smoother is the reference's Gauss-Seidel (multigrid.hpp:58, multigrid.cpp:29-31)
+    with pytest.raises(RuntimeError, match="gauss_seidel: zero diagonal at row 1"):
         hz.run_cycle(d.standard_plan(2, d.CycleKind.V, 1, 1), np.ones(2))
     assert d.MultigridHierarchy.from_levels(lv).levels() == 1
     with pytest.raises(RuntimeError, match="bad corner triple"):
@@ -258,7 +261,7 @@ def test_from_levels_matches_from_base():
         levels.append(lv)
     h = d.MultigridHierarchy.from_levels(levels)
     b = o.project(o.rhs("uniform", 3))
-    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     plan.cycles = 5
     res = h.run_cycle(plan, b)
     ox, oh = o.run_cycles(b, ncycles=5)
@@ -284,7 +287,7 @@ def test_config4_full_size(nsub):
     Bp = h.project_compatible(B)
     np.testing.assert_allclose(Bp[:, 0], B0, rtol=0, atol=1e-15)
     Bp[:, 0] = B0
-    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     plan.cycles = 2
     res = h.run_cycle(plan, Bp)
     ox, oh = o.run_cycles(B0, ncycles=2)
@@ -310,13 +313,13 @@ def test_config5_full_size(base, nsub, dirichlet, rhs):
     ob = o.rhs(rhs, 7)
     np.testing.assert_array_equal(b, ob)
     bp = ob if dirichlet else o.project(ob)
-    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     plan.cycles = 2
     res = h.run_cycle(plan, bp)
     ox, oh = o.run_cycles(bp, ncycles=2)
     np.testing.assert_array_equal(res.x, ox)
     assert np.all(np.abs(res.residual_history - oh) <= RTOL_HIST * oh)
-    rep = d.gmg_solve(h, d.standard_plan(h.levels(), d.CycleKind.V, 2, 2), b, 1e-8, 200)
+    rep = d.gmg_solve(h, d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi)), b, 1e-8, 200)
     assert rep.converged and rep.final_relative_residual <= 1e-8
     hist = np.array(rep.residual_history)
     assert np.all(hist[1:] < hist[:-1])
@@ -331,7 +334,7 @@ def test_odd_batch_widths_bitwise(nrhs):
     h = d.MultigridHierarchy.from_base(base, nsub, max_nrhs=nrhs)
     o = OracleHierarchy(base, nsub)
     B = np.stack([o.project(o.rhs("uniform", 40 + j)) for j in range(nrhs)], axis=1)
-    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     plan.cycles = 3
     res = h.run_cycle(plan, B)
     for j in range(nrhs):
@@ -348,7 +351,7 @@ def test_warm_start_and_cycle_cap():
     o = OracleHierarchy(base, nsub)
     b = o.rhs("uniform", 8)
     x0 = np.random.default_rng(1).uniform(-1, 1, h.n())
-    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     bp = o.project(b)
     plan.cycles = 3
     res = h.run_cycle(plan, bp, x0)
@@ -367,14 +370,14 @@ def test_w_cycle_solve_and_one_level_solve():
     h = d.MultigridHierarchy.from_base("equi:4:8:1.0", 3)
     o = OracleHierarchy("equi:4:8:1.0", 3)
     b = o.rhs("lr", 23)
-    plan = d.standard_plan(h.levels(), d.CycleKind.W, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.W, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     rep = d.gmg_solve(h, plan, b, 1e-10, 50)
     assert rep.converged
     bp = o.project(b)
     ox, oh = o.run_cycles(bp, ncycles=rep.iterations, walk=plan.walk_string())
     np.testing.assert_array_equal(rep.solution, ox)
     one = d.MultigridHierarchy.from_base("equi:4:8:1.0", 0)
-    rep1 = d.gmg_solve(one, d.standard_plan(1, d.CycleKind.V), one.make_rhs("lr", 5), 1e-12, 3)
+    rep1 = d.gmg_solve(one, d.standard_plan(1, d.CycleKind.V, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi)), one.make_rhs("lr", 5), 1e-12, 3)
     assert rep1.iterations == 1 and rep1.final_relative_residual <= 1e-12
 
 
@@ -389,13 +392,14 @@ def test_setup_errors_match_reference_messages():
         d.MultigridHierarchy.from_base((Q, np.array([[0, 1, 2]])), 0)
 
 
-@pytest.mark.parametrize("env", [{"DECMG_FUSE_RR": "1"}, {"DECMG_RR_WINDOW": "1"}, {"DECMG_KERNEL": "ell"},
-                                 {"DECMG_SWEEP2": "1"}, {"DECMG_PF": "0"}, {"DECMG_RPT": "2"}])
+@pytest.mark.parametrize("env", [{"DECMG_KERNEL": "ell"}, {"DECMG_KERNEL": "pipe"}, {"DECMG_PF": "0"},
+                                 {"DECMG_RPT": "2"}, {"DECMG_VTAIL": "0"}])
 @pytest.mark.parametrize("base,nsub,dirichlet,nrhs", [("ico", 6, False, 16), ("square", 6, True, 1)])
 def test_kernel_variants_bitwise(monkeypatch, env, base, nsub, dirichlet, nrhs):
-    """Every opt-in kernel variant (fused residual-restriction, high-occupancy
-    row kernel, fused sweep pairs, no prefetch, 2 RHS per thread) gives the
-    reference iterate bit for bit. The switches are read at context creation."""
+    """Every kernel switch (high-occupancy or pipelined row kernel for every
+    operator, no prefetch, 2 RHS per thread, per-pass kernels instead of the
+    bottom-of-V kernel) gives the reference iterate bit for bit. The switches
+    are read at context creation."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     h = d.MultigridHierarchy.from_base(base, nsub, dirichlet=dirichlet, max_nrhs=nrhs)
@@ -406,7 +410,7 @@ def test_kernel_variants_bitwise(monkeypatch, env, base, nsub, dirichlet, nrhs):
         B = h.make_rhs("uniform", 40, nrhs)
     if not dirichlet:
         B = np.stack([o.project(B[:, j]) for j in range(nrhs)], axis=1)
-    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     plan.cycles = 3
     res = h.run_cycle(plan, B if nrhs > 1 else B[:, 0])
     x = res.x if nrhs > 1 else res.x[:, None]
@@ -479,7 +483,7 @@ def test_cubic_hierarchy_vs_oracle(base, nsub, dirichlet):
     b = o.rhs("sinsin" if dirichlet else "uniform", 9)
     if not dirichlet:
         b = o.project(b)
-    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     plan.cycles = 3
     res = h.run_cycle(plan, b)
     ox, oh = o.run_cycles(b, ncycles=3)

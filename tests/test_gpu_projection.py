@@ -80,30 +80,35 @@ def test_projection_across_passes_and_solve_staging():
     check(h, o, B)
     assert h.projection_fallbacks() < 0.04 * (-(-h.n() // 32) * nrhs)
     Bp = np.stack([o.project(B[:, j].copy()) for j in range(nrhs)], axis=1)
-    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     plan.cycles = 1
     res = h.run_cycle(plan, Bp)
     rep = d.gmg_solve(h, plan, B, 1e-30, 1)
     np.testing.assert_array_equal(rep.solution, res.x)
 
 
-@pytest.mark.parametrize("nsub,nrhs", [(6, 16), (6, 5), (7, 1)])
-def test_wavefront_sweep_pairs_bitwise(monkeypatch, nsub, nrhs):
-    """The opt-in wavefront sweep pairs (csrc/pair.cu, DECMG_PAIR=1) give the
-    iterates of separate sweeps bit for bit (V(2,2): every post-smoothing pair
-    and the level-0 pre-smoothing pair with its fused residual norm)."""
-    plan_cycles = 3
-    out = {}
-    for flag in ("0", "1"):
-        monkeypatch.setenv("DECMG_PAIR", flag)
-        h = d.MultigridHierarchy.from_base("ico", nsub, max_nrhs=nrhs)
-        B = h.project_compatible(h.make_rhs("uniform", 4, nrhs))
-        plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
-        plan.cycles = plan_cycles
-        res = h.run_cycle(plan, B)
-        out[flag] = (res.x, np.asarray(res.residual_history))
-    np.testing.assert_array_equal(out["1"][0], out["0"][0])
-    np.testing.assert_allclose(out["1"][1], out["0"][1], rtol=1e-13, atol=0)
+@pytest.mark.parametrize("pre,post", [(2, 1), (1, 0), (2, 2), (0, 1), (3, 2)])
+def test_graph_solve_any_sweep_parity(monkeypatch, pre, post):
+    """gmg_solve's device loop (a CUDA graph replaying one captured cycle) is
+    used only when a cycle keeps level 0's ping-pong parity; V(2,1), V(1,0),
+    ... (an odd number of level-0 Jacobi sweeps) fall back to the host loop.
+    Either way: the oracle's cycle count and iterate, history within 1e-10."""
+    h = d.MultigridHierarchy.from_base("ico", 5)
+    o = OracleHierarchy("ico", 5)
+    b = h.make_rhs("uniform", 3)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, pre, post,
+                           smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
+    reps = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("DECMG_GRAPH", flag)
+        hh = d.MultigridHierarchy.from_base("ico", 5)
+        reps[flag] = [d.gmg_solve(hh, plan, b, 1e-8, 60) for _ in range(2)]  # 2nd call: cached graph
+    ox, ohist, oit, _ = o.solve(b, tol=1e-8, max_cycles=60, pre=pre, post=post)
+    for rep in reps["1"] + reps["0"]:
+        assert rep.iterations == oit
+        np.testing.assert_array_equal(rep.solution, ox)
+        np.testing.assert_allclose(rep.residual_history, ohist, rtol=1e-10, atol=0)
+    del h
 
 
 @pytest.mark.parametrize("base,nsub,dirichlet,nrhs", [("ico", 7, False, 4), ("square", 6, True, 1)])
@@ -111,7 +116,7 @@ def test_solve_batches_equal_single_solves(base, nsub, dirichlet, nrhs):
     """decmg_gpu_solve_batches: each batch of the pipelined stream gives the
     bits of its own gmg_solve (solution, history, cycle counts)."""
     h = d.MultigridHierarchy.from_base(base, nsub, dirichlet=dirichlet, max_nrhs=nrhs)
-    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     kinds = ["uniform", "lr", "uniform"] if not dirichlet else ["uniform", "sinsin", "lr"]
     batches = [h.make_rhs(k, 10 + i, nrhs) if nrhs > 1 else h.make_rhs(k, 10 + i) for i, k in enumerate(kinds)]
     reps = d.gmg_solve_batches(h, plan, batches, 1e-8, 60)
@@ -132,8 +137,8 @@ def test_device_solve_loop_matches_host_loop(monkeypatch):
     for flag in ("0", "1"):
         monkeypatch.setenv("DECMG_GRAPH", flag)
         h = d.MultigridHierarchy.from_base("ico", 7, max_nrhs=8)
-        v22 = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
-        w11 = d.standard_plan(h.levels(), d.CycleKind.W, 1, 1)
+        v22 = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
+        w11 = d.standard_plan(h.levels(), d.CycleKind.W, 1, 1, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
         out = []
         for plan, kind, nrhs, seed in [(v22, "uniform", 8, 1), (v22, "uniform", 3, 2), (w11, "lr", 8, 3),
                                        (v22, "uniform", 8, 4), (v22, "ylm", 1, 5)]:
@@ -152,7 +157,7 @@ def test_solve_batches_edges():
     """Batch streams: no batches, a cycle cap of 0 (the solution is x0 = 0 and
     the residual is reported) and of 1, and a null right-hand side."""
     h = d.MultigridHierarchy.from_base("ico", 5, max_nrhs=2)
-    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     assert d.gmg_solve_batches(h, plan, [], 1e-8, 10) == []
     b = h.make_rhs("uniform", 2, 2)
     for cap in (0, 1):
@@ -185,7 +190,7 @@ def test_bottom_of_v_kernel_bitwise(monkeypatch, base, nsub, dirichlet, nrhs, ki
         b = h.make_rhs("uniform", 6, nrhs) if nrhs > 1 else h.make_rhs("uniform", 6)
         if not dirichlet:
             b = h.project_compatible(b)
-        plan = d.standard_plan(h.levels(), getattr(d.CycleKind, kind), 2, 2)
+        plan = d.standard_plan(h.levels(), getattr(d.CycleKind, kind), 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
         plan.cycles = 3
         res = h.run_cycle(plan, b)
         rep = d.gmg_solve(h, plan, b, 1e-9, 30)

@@ -105,7 +105,7 @@ PCG = sorted(p.stem for p in GOLDEN.glob("pcg_*.json"))
 def w_walk(levels):
     """standard_plan's W walk (multigrid.cpp:149-194, emit_solve with gamma 2)."""
     import paper_2508_12501_b200 as d
-    return d.standard_plan(levels, d.CycleKind.W, 1, 1).walk_string()
+    return d.standard_plan(levels, d.CycleKind.W, 1, 1, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi)).walk_string()
 
 
 @pytest.mark.parametrize("stem", PCG)

@@ -52,7 +52,7 @@ for name in (sys.argv[1:] or list(CONFIGS)):
     setup = time.perf_counter() - t0
     n = h.n()
     B = h.make_rhs(kind, 1, nrhs) if nrhs > 1 else h.make_rhs(kind, 1)
-    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+    plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
     ps, keep = _plan_struct(plan, h.levels())
     Bd = torch.from_numpy(h.project_compatible(B) if not dirichlet else B).reshape(n, nrhs).cuda()
     Xd = torch.empty_like(Bd)

@@ -14,7 +14,7 @@ nsub = int(sys.argv[1]) if len(sys.argv) > 1 else 10
 nrhs = 16
 h = d.MultigridHierarchy.from_base("ico", nsub, max_nrhs=nrhs)
 B = h.project_compatible(h.make_rhs("uniform", 1, nrhs))
-plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
 plan.cycles = 2
 h.run_cycle(plan, B)
 cudart = C.CDLL("libcudart.so.12")

@@ -14,7 +14,7 @@ h = d.MultigridHierarchy.from_base(base, nsub, dirichlet=(base == "square"))
 b = h.make_rhs("uniform", 1)
 if base != "square":
     b = h.project_compatible(b)
-plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
 plan.cycles = 2
 h.run_cycle(plan, b)
 cudart = C.CDLL("libcudart.so.12")

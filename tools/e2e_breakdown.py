@@ -18,7 +18,7 @@ B = h.make_rhs("uniform", 1, nrhs)
 hb = torch.from_numpy(B).pin_memory()
 hx = torch.empty_like(hb).pin_memory()
 db = torch.empty(hb.shape, dtype=torch.float64, device="cuda")
-plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
 for rep in range(3):
     torch.cuda.synchronize()
     t0 = time.perf_counter()

@@ -14,7 +14,7 @@ import paper_2508_12501_b200 as d  # noqa: E402
 nsub = int(sys.argv[1]) if len(sys.argv) > 1 else 10
 h = d.MultigridHierarchy.from_base("ico", nsub, max_nrhs=16)
 B = torch.from_numpy(h.make_rhs("uniform", 1, 16)).pin_memory().numpy()
-plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
 ts = []
 for _ in range(8):
     t0 = time.perf_counter()

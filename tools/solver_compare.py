@@ -38,7 +38,7 @@ for name, m in [("jacobi", d.Smoother.WeightedJacobi), ("gs", d.Smoother.GaussSe
         t = time.perf_counter() - t0
     print(f"gmg_solve {name:7s} cycles {its.max():3d}  time to 1e-8 {1e3 * t:7.1f} ms  "
           f"final {fin.max():.2e}  {n * nrhs * its.max() / t / 1e9:.2f} G unknowns*cycles/s")
-plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2)
+plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
 ps, keep = _plan_struct(plan, h.levels())
 for rep in range(2):
     t0 = time.perf_counter()

@@ -10,7 +10,7 @@ for base, dirich, nsub in (("square", True, 11), ("square", True, 12), ("ico", F
     b = o.rhs("uniform", 3)
     if not dirich: b = o.project(b)
     for cyc in (1, 2):
-        plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2); plan.cycles = cyc
+        plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi)); plan.cycles = cyc
         x = h.run_cycle(plan, b).x
         ox, oh = o.run_cycles(b, ncycles=cyc)
         diff = np.flatnonzero(x != ox)
