@@ -11,10 +11,14 @@ as 16 x 10,485,762 unknowns).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun, one process per GPU): the same workload partitioned across
-the GPUs by vertex (Morton-key ranges, 1-ring halos exchanged with NCCL
-grouped send/recv, coarse levels replicated) -- strong
-scaling of the fixed problem; the cycle time is the max over ranks.
+N > 1 (torchrun, one process per GPU): BASELINE config 5b (icosphere x11,
+41,943,042 vertices, one RHS) partitioned across the GPUs by vertex
+(contiguous Morton ranges, 1-ring halos exchanged with NCCL grouped
+send/recv behind the interior rows, coarse levels replicated, cycles replayed
+as CUDA graphs) -- strong scaling of the fixed problem; the
+cycle time is the max over ranks. At N = 1 the same partitioned path runs
+config 5b after the headline and is reported as `scale_config` (the base of
+the scaling curve).
 `--impl reference` times the reference's CPU solver (oracle/_ref, the
 reference compiled in place) on a bounded sample on the host cores.
 
@@ -344,7 +348,7 @@ def run_ours(args, world, rank, local):
            "cycles_to_1e-8": single_done, "final_rel_residual_max": float(bfin.max())}
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+           "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": f"BASELINE config 4: icosphere x{args.nsub} ({n} vertices, {levels} levels), "
                                   f"{args.nrhs} RHS batch, weighted-Jacobi V(2,2), coarse CG, fp64",
@@ -357,36 +361,48 @@ def run_ours(args, world, rank, local):
            "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_port()
+    h.close()
+    if world == 1 and not args.no_scale_config:
+        # the N = 1 point of the multi-GPU scaling workload (config 5b through the
+        # same partitioned path `--gpus N` runs), so SCALE's N > 1 lines have a base
+        sc = run_partitioned(args, world, rank, local)
+        out["scale_config"] = {k: sc[k] for k in ("value", "unit", "ms_per_step", "n_gpus", "steps", "scaling",
+                                                  "config", "roofline", "e2e", "gpu_launches")}
     if rank == 0:
         print(json.dumps(out), flush=True)
 
 
 # ------------------------------------------------------------ partitioned ----
+SCALE_NSUB = 11  # BASELINE config 5b: icosphere x11, 41,943,042 vertices, single RHS
+
+
 def run_partitioned(args, world, rank, local):
+    """BASELINE config 5b through the vertex-partitioned path:
+    one rank per GPU (NCCL; N = 1 is the same path without peers), K V(2,2)
+    weighted-Jacobi cycles with the fine residual after each, timed on the
+    device inside the library (max over ranks). Strong scaling: the problem is
+    fixed, N GPUs share it."""
     import torch
-    import torch.distributed as dist
 
     import paper_2508_12501_b200 as d
 
     torch.cuda.set_device(local)
     uid = share_nccl_id(world, rank, d.nccl_unique_id)
     t0 = time.perf_counter()
-    dh = d.DistributedHierarchy("ico", args.nsub, world, rank=rank, nccl_id=uid, device=local,
-                                max_nrhs=args.nrhs)
+    dh = d.DistributedHierarchy("ico", args.scale_nsub, world, rank=rank, nccl_id=uid, device=local, max_nrhs=1,
+                                agglomerate_below=args.agglomerate)
     setup_s = time.perf_counter() - t0
     g = dh.context()
     n = g.n()
     levels = dh.levels()
-    plan = d.standard_plan(levels, d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi))
-    B = g.make_rhs("uniform", SEED0, args.nrhs)  # the same batch as the 1-GPU run
-    Bp = g.project_compatible(B)
-    hb = torch.from_numpy(Bp).pin_memory().numpy()
-    # warm-up, then K steps (one run of K cycles); cycle-loop time by CUDA events in the library
+    jac = d.SmootherConfig(d.Smoother.WeightedJacobi)
+    plan = d.standard_plan(levels, d.CycleKind.V, 2, 2, smoother=jac)
+    b = g.make_rhs("uniform", SEED0)
+    bp = g.project_compatible(b)
+    hb = torch.from_numpy(bp).pin_memory().numpy()
     plan.cycles = args.warmup
-    dh.run_cycle(plan, hb)
+    dh.run_cycle(plan, hb)  # warm-up (also captures the cycle graph)
     plan.cycles = args.steps
-    g.set_timing(True)
-    g.timing(-1)
     launches0 = dh.launch_count()
     with ClockSampler(local) as clk:
         barrier(world)
@@ -394,40 +410,49 @@ def run_partitioned(args, world, rank, local):
         barrier(world)
     ms = max_over_ranks(world, dh.last_cycle_ms())
     launches = dh.launch_count() - launches0
+    value = float(n) * args.steps / (ms / 1e3)
+    # kernel breakdown: the same K cycles again, eager, events around every launch
+    g.set_timing(True)
+    g.timing(-1)
+    dh.run_cycle(plan, hb)
     cls = {c: g.timing(c) for c in range(8)}
     g.set_timing(False)
-    value = float(n) * args.nrhs * args.steps / (ms / 1e3)
     nl, tms, tbytes = cls[0]
     peak, peak_kind = measured_peak()
     achieved = (tbytes / max(nl, 1)) / (tms / max(nl, 1) / 1e3) / 1e9 if nl else None
-    roofline = {"bound": "hbm", "kernel": "k_rowop_pipe<16,4,W,OP_SWEEP> (level-0 sweep, this rank's rows)",
+    roofline = {"bound": "hbm", "kernel": "k_rowop_pipe<1,1,7,OP_SWEEP> (level-0 sweep of this rank's rows)",
                 "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None, "traffic": None,
-                "algorithmic_bytes_per_launch": tbytes / max(nl, 1), "launches": nl}
+                "algorithmic_bytes_per_launch": tbytes / max(nl, 1), "launches": nl,
+                "classes_ms": {k: round(v[1], 4) for k, v in zip(
+                    ["fine_sweep", "fine_residual", "restrict", "prolong", "coarse_levels", "coarse_solve",
+                     "norms", "zero_start_sweeps"], cls.values())}}
     # e2e: gmg_solve to 1e-8 from pinned host memory to pinned host memory
-    hB = torch.from_numpy(B).pin_memory().numpy()
-    dh.gmg_solve(d.standard_plan(levels, d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi)), hB, 1e-8, 200)
+    hB = torch.from_numpy(b).pin_memory().numpy()
+    dh.gmg_solve(plan, hB, 1e-8, 200)
     barrier(world)
     t0 = time.perf_counter()
-    rep = dh.gmg_solve(d.standard_plan(levels, d.CycleKind.V, 2, 2, smoother=d.SmootherConfig(d.Smoother.WeightedJacobi)), hB, 1e-8, 200)
+    rep = dh.gmg_solve(plan, hB, 1e-8, 200)
     e2e_s = max_over_ranks(world, time.perf_counter() - t0)
-    cyc = sum(rep.iterations)
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"BASELINE config 4: icosphere x{args.nsub} ({n} vertices, {levels} levels), "
-                                  f"{args.nrhs} RHS batch, weighted-Jacobi V(2,2), coarse CG, fp64, vertex-partitioned",
-                      "vertices": n, "levels": levels, "nrhs": args.nrhs, "global_batch": args.nrhs,
-                      "parallelism": f"vertex partition x{world} (Morton-key ranges, NCCL halo exchange, "
-                                     f"levels >= {dh.agglomeration_level} replicated)",
+           "config": {"workload": f"BASELINE config 5b: icosphere x{args.scale_nsub} ({n} vertices, {levels} levels), "
+                                  f"single seeded uniform(-1,1) RHS, weighted-Jacobi V(2,2), coarse CG, fp64, "
+                                  f"vertex-partitioned over {world} GPU(s)",
+                      "vertices": n, "levels": levels, "nrhs": 1, "global_batch": 1,
+                      "parallelism": f"vertex partition x{world} (contiguous Morton ranges, 1-ring halos over NCCL "
+                                     f"overlapping the interior rows, levels >= {dh.agglomeration_level} replicated)",
                       "owned_rows_rank0": dh.owned0, "halo_rows_rank0": dh.halo0, "setup_s": setup_s,
-                      "l2": "vectors >> 126 MB L2", "last_step_rel_residual_max": float(np.max(res.residual_history[-1]))},
+                      "l2": "level-0 vectors 336 MB >> 126 MB L2 (no flush needed)",
+                      "last_step_rel_residual": float(np.max(res.residual_history[-1]))},
            "roofline": roofline,
-           "e2e": {"value": float(n) * cyc / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(B.nbytes),
-                   "d2h_bytes_per_step": int(B.nbytes), "time_to_1e-8_s": e2e_s, "cycles_to_1e-8": rep.iterations},
+           "e2e": {"value": float(n) * rep.iterations / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(b.nbytes),
+                   "d2h_bytes_per_step": int(b.nbytes), "time_to_1e-8_s": e2e_s, "cycles_to_1e-8": rep.iterations,
+                   "step": "one gmg_solve(tol=1e-8) from pinned host memory to pinned host memory"},
            "gpu_launches": int(launches), "clocks": clk.summary()}
-    if rank == 0:
-        print(json.dumps(out), flush=True)
+    dh.close()
+    return out
 
 
 # ------------------------------------------------------------- reference ----
@@ -480,7 +505,11 @@ def main():
     ap.add_argument("--ref-nsub", type=int, default=9)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partitioned", action="store_true",
-                    help="use the vertex-partitioned NCCL path even at N = 1 (plumbing check)")
+                    help="print the config-5b partitioned line at N = 1 instead of the config-4 headline")
+    ap.add_argument("--scale-nsub", type=int, default=SCALE_NSUB)
+    ap.add_argument("--agglomerate", type=int, default=65536,
+                    help="replicate levels with fewer vertices per rank than this")
+    ap.add_argument("--no-scale-config", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -488,7 +517,9 @@ def main():
     if args.impl == "reference":
         run_reference(args, world, rank)
     elif world > 1 or args.partitioned:
-        run_partitioned(args, world, rank, local)
+        out = run_partitioned(args, world, rank, local)
+        if rank == 0:
+            print(json.dumps(out), flush=True)
     else:
         run_ours(args, world, rank, local)
     if world > 1:

@@ -216,16 +216,36 @@ DECMG_API int decmg_gpu_make_rhs(decmg_gpu_ctx* ctx, const char* kind, uint64_t 
 
 
 /* ---- Vertex-partitioned multi-GPU V-cycle ----
- * Every rank builds the full hierarchy; levels with >= agglomerate_below
- * vertices per rank are partitioned by Morton-key ranges with 1-ring halos
- * (NCCL grouped send/recv), coarser levels run replicated on every rank.
- * Iterates are bit-identical to the single-GPU solve for any rank count.
- * nccl_id == NULL: emulate world_size ranks inside this process on
- * cfg->device (device copies instead of NCCL; used by the parity tests).
- * Otherwise one process per GPU: rank in [0, world_size), nccl_id = the
- * 128-byte ncclUniqueId from decmg_gpu_nccl_unique_id on rank 0. */
+ * The reference has no distribution; this is the north star's
+ * "vertex set partitioned across 1/2/4/8 GPUs". Every rank builds the full
+ * hierarchy; level-0 vertices are split into contiguous ranges of the Morton
+ * row order (coarse vertices follow their fine copies); levels with >=
+ * agglomerate_below vertices per rank are partitioned with 1-ring halos,
+ * coarser levels run replicated on every rank. Iterates are bit-identical to
+ * the single-GPU solve for any rank count; residual histories agree within
+ * rounding (per-rank partial sums added in rank order).
+ * Transports:
+ *   DECMG_DIST_EMULATE  all world_size ranks inside this process on
+ *                       cfg->device (device copies; rank is ignored)
+ *   DECMG_DIST_NCCL     one process per GPU; nccl_id = the 128-byte
+ *                       ncclUniqueId from decmg_gpu_nccl_unique_id on rank 0
+ *   DECMG_DIST_SHM      one process per rank, host-staged halos through the
+ *                       file shm_path (same path on every rank, e.g. under
+ *                       /dev/shm; created if absent, must start empty) with a
+ *                       host barrier; ranks may share one GPU. */
 typedef struct decmg_gpu_dist decmg_gpu_dist;
+enum { DECMG_DIST_EMULATE = 0, DECMG_DIST_NCCL = 1, DECMG_DIST_SHM = 2 };
+typedef struct {
+    int kind;
+    const void* nccl_id;
+    const char* shm_path;
+} decmg_gpu_dist_transport;
 DECMG_API int decmg_gpu_nccl_unique_id(void* out, int bytes);
+DECMG_API int decmg_gpu_dist_create_ex(const double* positions, int nv, const int* corner_triples, int nt, int nsub,
+                                       unsigned flags, const decmg_gpu_config* cfg, int world_size, int rank,
+                                       const decmg_gpu_dist_transport* transport, int agglomerate_below,
+                                       decmg_gpu_dist** out);
+/* nccl_id == NULL: emulation; otherwise NCCL (decmg_gpu_dist_create_ex). */
 DECMG_API int decmg_gpu_dist_create(const double* positions, int nv, const int* corner_triples, int nt, int nsub,
                                     unsigned flags, const decmg_gpu_config* cfg, int world_size, int rank,
                                     const void* nccl_id, int agglomerate_below, decmg_gpu_dist** out);
@@ -233,17 +253,17 @@ DECMG_API void decmg_gpu_dist_destroy(decmg_gpu_dist* d);
 DECMG_API const char* decmg_gpu_dist_last_error(const decmg_gpu_dist* d);
 DECMG_API int decmg_gpu_dist_info(const decmg_gpu_dist* d, int* agglomeration_level, int* levels, int64_t* owned0,
                                   int64_t* halo0);
-/* run_cycle (solve == 0, ncycles = max_cycles) or gmg_solve (solve != 0) with
- * full-length host vectors replicated on every rank; x_out receives the full
- * solution on every rank. */
-/* CUDA-event time of the last decmg_gpu_dist_run's cycle loop on this rank
- * (cycles + per-cycle residual norms; excludes input staging, projection and
- * the solution gather), and the kernel launches of this rank so far. */
 /* The full (replicated) hierarchy of this rank: every single-context entry
  * point (make_rhs, export, apply, timing, ...) works on it; owned by d. */
 DECMG_API decmg_gpu_ctx* decmg_gpu_dist_context(decmg_gpu_dist* d);
+/* CUDA-event time of the last decmg_gpu_dist_run's cycle loop on this rank
+ * (cycles + per-cycle residual norms; excludes input staging, projection and
+ * the solution gather), and the kernel launches of this rank so far. */
 DECMG_API double decmg_gpu_dist_last_cycle_ms(const decmg_gpu_dist* d);
 DECMG_API int64_t decmg_gpu_dist_launch_count(const decmg_gpu_dist* d);
+/* run_cycle (solve == 0, ncycles = max_cycles) or gmg_solve (solve != 0) with
+ * full-length host vectors replicated on every rank; x_out receives the full
+ * solution on every rank. Weighted Jacobi only. */
 DECMG_API int decmg_gpu_dist_run(decmg_gpu_dist* d, const decmg_gpu_plan* plan, int nrhs, const double* b,
                                  const double* x0, int max_cycles, int solve, double tol, double* x_out,
                                  double* hist_out, int* cycles_done, double* final_out);

@@ -43,6 +43,15 @@ class decmg_gpu_plan(C.Structure):
                 ("jacobi_omega", C.c_double)]
 
 
+class decmg_gpu_dist_transport(C.Structure):
+    _fields_ = [("kind", C.c_int), ("nccl_id", C.c_void_p), ("shm_path", C.c_char_p)]
+
+
+DECMG_DIST_EMULATE = 0
+DECMG_DIST_NCCL = 1
+DECMG_DIST_SHM = 2
+
+
 class decmg_gpu_level_desc(C.Structure):
     _fields_ = [("nv", C.c_int),
                 ("L_row_ptr", C.c_void_p), ("L_col_idx", C.c_void_p), ("L_values", C.c_void_p),
@@ -94,6 +103,9 @@ SIGNATURES = {
     "decmg_gpu_dist_create": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_uint,
                                         C.POINTER(decmg_gpu_config), C.c_int, C.c_int, C.c_void_p, C.c_int,
                                         C.POINTER(C.c_void_p)]),
+    "decmg_gpu_dist_create_ex": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_uint,
+                                           C.POINTER(decmg_gpu_config), C.c_int, C.c_int,
+                                           C.POINTER(decmg_gpu_dist_transport), C.c_int, C.POINTER(C.c_void_p)]),
     "decmg_gpu_dist_destroy": (None, [C.c_void_p]),
     "decmg_gpu_dist_last_error": (C.c_char_p, [C.c_void_p]),
     "decmg_gpu_dist_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int64),

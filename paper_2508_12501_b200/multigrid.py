@@ -529,15 +529,18 @@ def gmg_preconditioned_cg(h: MultigridHierarchy, inner_plan: CyclePlan, b: np.nd
 class DistributedHierarchy:
     """Vertex-partitioned multi-GPU hierarchy.
 
-    world_size ranks; with nccl_id=None all ranks are emulated in this process
-    on one device (device copies instead of NCCL -- the parity tests), else
-    this process is `rank` of a one-process-per-GPU job and nccl_id is the
-    128-byte id from `nccl_unique_id()` on rank 0.
+    world_size ranks. Transports (include/decmg_gpu.h):
+      * nccl_id=None, shm_path=None: all ranks emulated in this process on one
+        device (device copies instead of NCCL);
+      * nccl_id: this process is `rank` of a one-process-per-GPU job and
+        nccl_id is the 128-byte id from `nccl_unique_id()` on rank 0;
+      * shm_path: this process is `rank`, halos host-staged through the shared
+        file shm_path (several ranks may share one GPU: the multi-process test).
     """
 
     def __init__(self, base, nsub: int, world_size: int, rank: int = 0, nccl_id: Optional[bytes] = None,
                  dirichlet: bool = False, project_sphere: Optional[bool] = None, device: int = 0, max_nrhs: int = 1,
-                 agglomerate_below: int = 65536):
+                 agglomerate_below: int = 65536, shm_path: Optional[str] = None):
         self._lib = _lib.load()
         if isinstance(base, str):
             if project_sphere is None:
@@ -551,9 +554,15 @@ class DistributedHierarchy:
         cfg = decmg_gpu_config(device=device, max_nrhs=max_nrhs)
         out = C.c_void_p()
         idbuf = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), len(nccl_id))
-        check(self._lib.decmg_gpu_dist_create(_ptr(pos), pos.shape[0], _ptr(tri), tri.shape[0], nsub, flags,
-                                              C.byref(cfg), world_size, rank, idbuf, agglomerate_below,
-                                              C.byref(out)), None, dist=True)
+        if nccl_id is not None:
+            tr = _lib.decmg_gpu_dist_transport(_lib.DECMG_DIST_NCCL, C.cast(idbuf, C.c_void_p), None)
+        elif shm_path is not None:
+            tr = _lib.decmg_gpu_dist_transport(_lib.DECMG_DIST_SHM, None, str(shm_path).encode())
+        else:
+            tr = _lib.decmg_gpu_dist_transport(_lib.DECMG_DIST_EMULATE, None, None)
+        check(self._lib.decmg_gpu_dist_create_ex(_ptr(pos), pos.shape[0], _ptr(tri), tri.shape[0], nsub, flags,
+                                                 C.byref(cfg), world_size, rank, C.byref(tr), agglomerate_below,
+                                                 C.byref(out)), None, dist=True)
         self._d = out
         self.world_size = world_size
         self.dirichlet = dirichlet
