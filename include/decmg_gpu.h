@@ -51,6 +51,7 @@ enum {
 #define DECMG_PROJECT_SPHERE 1u /* push new midpoints to the unit sphere (x2)   */
 #define DECMG_DIRICHLET 2u      /* identity rows on boundary vertices (x1)      */
 #define DECMG_CUBIC 4u          /* SubdivisionScheme::Cubic (1 -> 9, subdivision.cpp:116-120) instead of Binary */
+#define DECMG_CLAMP_DUAL_AREAS 8u /* HodgeOptions::clamp_dual_areas (operators.hpp:31-35, operators.cpp:80-114) */
 
 typedef struct {
     int device;   /* CUDA device ordinal                                    */
@@ -68,6 +69,13 @@ typedef struct {
 DECMG_API int decmg_gpu_create_from_base(const double* positions, int nv, const int* corner_triples, int nt,
                                int nsub, unsigned flags, const decmg_gpu_config* cfg,
                                decmg_gpu_ctx** out);
+
+/* The same with build_hierarchy's use_levels (multigrid.cpp:325-341): keep
+ * only the finest use_levels meshes of the tower (0 = all), so the coarse
+ * solve runs on a finer mesh. */
+DECMG_API int decmg_gpu_create_from_base_ex(const double* positions, int nv, const int* corner_triples, int nt,
+                                           int nsub, int use_levels, unsigned flags, const decmg_gpu_config* cfg,
+                                           decmg_gpu_ctx** out);
 
 /* Upload an already assembled hierarchy (reference layout: CSR of L per level,
  * P = prolongation n_k x n_{k+1}, R = restriction n_{k+1} x n_k, dual areas).
@@ -166,6 +174,21 @@ DECMG_API void* decmg_gpu_stream(decmg_gpu_ctx* ctx); /* cudaStream_t of the con
 
 /* MultigridHierarchy::project_compatible (proj/src/multigrid.cpp:240-250), in place. */
 DECMG_API int decmg_gpu_project_compatible(decmg_gpu_ctx* ctx, int nrhs, double* b);
+
+/* smooth (proj/include/decmg/multigrid.hpp:66-68, src/multigrid.cpp:95-120)
+ * with A = level k's Laplacian: iters sweeps of `smoother` (DECMG_SMOOTHER_*,
+ * omega for Jacobi) on x in place ([n_k][nrhs], reference numbering).
+ * weighted != 0: the CG smoother's inner product uses the level's dual areas
+ * (what cycle_once passes), else plain dots (smooth's default weights = {}).
+ * Errors as the reference: zero diagonal -> DECMG_RUNTIME. */
+DECMG_API int decmg_gpu_smooth(decmg_gpu_ctx* ctx, int level, int smoother, double omega, int iters, int nrhs,
+                               double* x, const double* b, int weighted);
+
+/* SolveReport::cumulative_seconds (proj/include/decmg/solvers.hpp:20) of the
+ * last decmg_gpu_solve / decmg_gpu_pcg on ctx: seconds since the call began
+ * at which each cycle's (iteration's) residual was known; for a batch, the
+ * cycles of the longest lane. Returns the count (query with out = NULL). */
+DECMG_API int decmg_gpu_last_times(const decmg_gpu_ctx* ctx, double* out, int max);
 
 /* SparseOperator::apply (proj/src/sparse.cpp:209-218) of level k's operator
  * op = 'L' (n_k x n_k), 'P' (n_k x n_{k+1}), 'R' (n_{k+1} x n_k). */

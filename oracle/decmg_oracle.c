@@ -914,6 +914,18 @@ static int smooth(const level_t* lv, double* x, const double* b, const plan_t* p
     return 0;
 }
 
+/* smooth(A = level k's Laplacian, x, b, cfg, iters, weights = dual areas)
+ * (proj/include/decmg/multigrid.hpp:66-68, proj/src/multigrid.cpp:95-120), x in place. */
+int orc_smooth(const orc_hier* h, int k, int smoother, double omega, int iters, const double* b, double* x) {
+    if (k < 0 || k >= h->L) { set_err("smooth: level out of range"); return -1; }
+    const level_t* lv = &h->lv[k];
+    double* s = NEW(double, lv->m.nv);
+    plan_t p = {0, 0, smoother, omega};
+    const int rc = smooth(lv, x, b, &p, iters, s);
+    free(s);
+    return rc;
+}
+
 /* MultigridHierarchy::cycle_once (proj/src/multigrid.cpp:252-285) with the
  * x1 extension (coarse RHS zeroed on Dirichlet vertices after restriction). */
 static int cycle_once(const orc_hier* h, const char* walk, const plan_t* p, double** xs, double** bs,

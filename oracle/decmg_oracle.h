@@ -58,6 +58,9 @@ int orc_solve(const orc_hier* h, int pre, int post, int smoother, double omega,
               const double* b, double tol, int max_cycles, double* x_out, double* hist_out,
               int* iters_out, double* final_out);
 void orc_coarse_solve(const orc_hier* h, const double* b, double* x);
+/* smooth (multigrid.cpp:95-120) on level k's Laplacian, x in place; smoother as above, 3 = cg_fixed
+ * with the level's dual areas as weights. Returns nonzero on a zero diagonal. */
+int orc_smooth(const orc_hier* h, int k, int smoother, double omega, int iters, const double* b, double* x);
 /* gmg_preconditioned_cg (proj/src/solvers.cpp:118-130): hist_out needs
  * maxiter + 1 entries; returns -2 on a CG breakdown (message in last_error). */
 int orc_pcg(const orc_hier* h, const char* walk, int pre, int post, int smoother, double omega, int ncycles,

@@ -8,9 +8,9 @@ reference's C++ multigrid API; it has no CPU implementation of the path.
 from ._lib import DecmgError, CudaError, LIB_PATH, load as load_library
 from .multigrid import (CycleKind, CyclePlan, CycleResult, DistributedHierarchy, MultigridHierarchy, Smoother,
                         SmootherConfig, SolveReport, Transition, base_mesh, build_hierarchy, gmg_preconditioned_cg,
-                        gmg_solve, gmg_solve_batches, nccl_unique_id, read_obj, standard_plan)
+                        gmg_solve, gmg_solve_batches, nccl_unique_id, read_obj, smooth, standard_plan)
 
 __all__ = ["CycleKind", "CyclePlan", "CycleResult", "DistributedHierarchy", "MultigridHierarchy", "nccl_unique_id", "Smoother", "SmootherConfig",
            "SolveReport", "Transition", "base_mesh", "build_hierarchy", "gmg_preconditioned_cg", "gmg_solve", "gmg_solve_batches",
-           "standard_plan", "read_obj",
+           "standard_plan", "read_obj", "smooth",
            "DecmgError", "CudaError", "LIB_PATH", "load_library"]

@@ -23,6 +23,7 @@ DECMG_OOM = 5
 DECMG_PROJECT_SPHERE = 1
 DECMG_DIRICHLET = 2
 DECMG_CUBIC = 4
+DECMG_CLAMP_DUAL_AREAS = 8
 
 
 class DecmgError(RuntimeError):
@@ -67,6 +68,8 @@ class decmg_gpu_level_desc(C.Structure):
 SIGNATURES = {
     "decmg_gpu_create_from_base": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_uint,
                                              C.POINTER(decmg_gpu_config), C.POINTER(C.c_void_p)]),
+    "decmg_gpu_create_from_base_ex": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                                C.c_uint, C.POINTER(decmg_gpu_config), C.POINTER(C.c_void_p)]),
     "decmg_gpu_create_from_levels": (C.c_int, [C.POINTER(decmg_gpu_level_desc), C.c_int, C.c_uint,
                                                C.POINTER(decmg_gpu_config), C.POINTER(C.c_void_p)]),
     "decmg_gpu_destroy": (None, [C.c_void_p]),
@@ -99,6 +102,9 @@ SIGNATURES = {
     "decmg_gpu_write_obj": (C.c_int, [C.c_void_p, C.c_int, C.c_char_p]),
     "decmg_gpu_write_matrix_market": (C.c_int, [C.c_void_p, C.c_int, C.c_char, C.c_char_p]),
     "decmg_gpu_make_rhs": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_int, C.c_void_p]),
+    "decmg_gpu_smooth": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_void_p,
+                                   C.c_void_p, C.c_int]),
+    "decmg_gpu_last_times": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     "decmg_gpu_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_int]),
     "decmg_gpu_dist_create": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_uint,
                                         C.POINTER(decmg_gpu_config), C.c_int, C.c_int, C.c_void_p, C.c_int,

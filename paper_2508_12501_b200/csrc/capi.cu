@@ -143,13 +143,18 @@ const char* decmg_gpu_last_error(const decmg_gpu_ctx* ctx) {
 int decmg_gpu_create_from_base(const double* positions, int nv, const int* corner_triples, int nt,
                                int nsub, unsigned flags, const decmg_gpu_config* cfg,
                                decmg_gpu_ctx** out) {
+    return decmg_gpu_create_from_base_ex(positions, nv, corner_triples, nt, nsub, 0, flags, cfg, out);
+}
+
+int decmg_gpu_create_from_base_ex(const double* positions, int nv, const int* corner_triples, int nt, int nsub,
+                                  int use_levels, unsigned flags, const decmg_gpu_config* cfg, decmg_gpu_ctx** out) {
     if (!out || !positions || !corner_triples)
         return fail(nullptr, Status::Err(DECMG_INVALID_ARGUMENT, "create_from_base: null argument"));
     *out = nullptr;
     auto* c = new decmg_gpu_ctx();
     c->flags = flags;
     Status s = init_ctx(c, cfg);
-    if (s.ok()) s = build_from_base(c, positions, nv, corner_triples, nt, nsub, flags);
+    if (s.ok()) s = build_from_base(c, positions, nv, corner_triples, nt, nsub, flags, use_levels);
     if (!s.ok()) {
         destroy_ctx(c);
         return fail(nullptr, s);
@@ -293,6 +298,40 @@ int decmg_gpu_project_compatible(decmg_gpu_ctx* ctx, int nrhs, double* b) {
     API_TRY(ctx, cuda_status(cudaMemcpyAsync(b, db.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H"));
     API_TRY(ctx, cuda_status(cudaStreamSynchronize(ctx->stream), "project"));
     return DECMG_OK;
+}
+
+int decmg_gpu_smooth(decmg_gpu_ctx* ctx, int level, int smoother, double omega, int iters, int nrhs, double* x,
+                     const double* b, int weighted) {
+    if (!ctx || !x || !b) return DECMG_INVALID_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    const int L = static_cast<int>(ctx->lv.size());
+    if (level < 0 || level >= L) return fail(ctx, Status::Err(DECMG_INVALID_ARGUMENT, "smooth: level out of range"));
+    decmg_gpu_plan ps{};
+    ps.smoother = smoother;
+    ps.jacobi_omega = omega;
+    ps.pre_all = ps.post_all = 0;
+    Plan p;
+    API_TRY(ctx, make_plan(ctx, &ps, &p));
+    if (nrhs < 1 || nrhs > ctx->max_nrhs)
+        return fail(ctx, Status::Err(DECMG_INVALID_ARGUMENT, "nrhs must be in [1, max_nrhs] (max 32)"));
+    const size_t n = static_cast<size_t>(ctx->lv[level].nv) * nrhs;
+    DevBuf dx, db;
+    API_TRY(ctx, dx.alloc(n));
+    API_TRY(ctx, db.alloc(n));
+    API_TRY(ctx, cuda_status(cudaMemcpyAsync(dx.p, x, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D"));
+    API_TRY(ctx, cuda_status(cudaMemcpyAsync(db.p, b, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D"));
+    API_TRY(ctx, smooth_level(ctx, level, p, iters, nrhs, dx.p, db.p, dx.p, weighted != 0));
+    API_TRY(ctx, cuda_status(cudaMemcpyAsync(x, dx.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H"));
+    API_TRY(ctx, cuda_status(cudaStreamSynchronize(ctx->stream), "smooth"));
+    return DECMG_OK;
+}
+
+int decmg_gpu_last_times(const decmg_gpu_ctx* ctx, double* out, int max) {
+    if (!ctx) return -1;
+    const int n = static_cast<int>(ctx->last_times.size());
+    if (out)
+        for (int i = 0; i < n && i < max; ++i) out[i] = ctx->last_times[i];
+    return n;
 }
 
 int decmg_gpu_apply(decmg_gpu_ctx* ctx, int level, char op, const double* x, double* y) {

@@ -161,6 +161,8 @@ struct decmg_gpu_ctx {
     double* bproj = nullptr;    // projected RHS for solve [n0][max_nrhs]
     double* xsol = nullptr;     // solve snapshot [n0][max_nrhs]
     double* hist_dev = nullptr; // [hist_cap][max_nrhs]
+    unsigned long long* tstamp_dev = nullptr;  // [hist_cap + 1] %globaltimer at the solve start / each check
+    std::vector<double> last_times;  // SolveReport::cumulative_seconds of the last solve / pcg
     int hist_cap = 0;
     double* io_b = nullptr;     // staging for host-pointer calls [n0][max_nrhs]
     double* io_x0 = nullptr;
@@ -267,7 +269,7 @@ inline unsigned grid_for(int64_t threads, int block) {
 
 // setup.cu
 Status build_from_base(decmg_gpu_ctx* c, const double* pos, int nv, const int* corners, int nt,
-                       int nsub, unsigned flags);
+                       int nsub, unsigned flags, int use_levels = 0);
 Status build_from_levels(decmg_gpu_ctx* c, const decmg_gpu_level_desc* levels, int nlevels,
                          unsigned flags);
 Status alloc_work(decmg_gpu_ctx* c);
@@ -297,5 +299,9 @@ Status pcg(decmg_gpu_ctx* c, const Plan& inner, int inner_cycles, int nrhs, cons
            int maxiter, double* d_x, double* h_hist, int* iters, int* converged, double* h_final, bool staged = false);
 Status project_compatible(decmg_gpu_ctx* c, int nrhs, double* d_b);
 Status apply_op(decmg_gpu_ctx* c, int level, char op, const double* d_x, double* d_y);
+// smooth (multigrid.cpp:95-120) on level k's operator; vectors in the reference numbering
+Status smooth_level(decmg_gpu_ctx* c, int k, const Plan& plan, int iters, int nrhs, const double* d_x,
+                    const double* d_b, double* d_out, bool weighted);
+Status build_gs_schedule(decmg_gpu_ctx* c, Level& m);
 
 }  // namespace decmg_gpu

@@ -261,19 +261,14 @@ Status solve_graph(decmg_gpu_ctx* c, Driver& dr, const Plan& plan, int nrhs, uns
     *graphed = false;
     if (!c->gstate_raw) DG_TRY(dalloc(c, &c->gstate_raw, (sizeof(SolveState) + 7) / 8));
     SolveState* gst = reinterpret_cast<SolveState*>(c->gstate_raw);
-    if (max_cycles > c->hist_cap) {
-        if (c->hist_dev) cudaFree(c->hist_dev);
-        c->hist_dev = nullptr;
-        c->hist_cap = 0;
-        DG_CUDA(cudaMalloc(&c->hist_dev, sizeof(double) * max_cycles * 32));
-        c->hist_cap = max_cycles;
-    }
+
     // omega by its exact bits: two omegas that print alike must not share a graph
     uint64_t omega_bits = 0;
     std::memcpy(&omega_bits, &plan.omega, sizeof omega_bits);
     std::string key = plan.walk + "|" + std::to_string(plan.smoother) + "|" + std::to_string(omega_bits) + "|" +
                       std::to_string(nrhs) + "|" + std::to_string(reinterpret_cast<uintptr_t>(dr.b0)) + "|" +
                       std::to_string(reinterpret_cast<uintptr_t>(c->hist_dev)) + "|" +
+                      std::to_string(reinterpret_cast<uintptr_t>(c->tstamp_dev)) + "|" +
                       std::to_string(reinterpret_cast<uintptr_t>(c->red)) + "|";
     for (size_t k = 0; k < c->lv.size(); ++k)
         key += std::to_string(plan.pre[k]) + "," + std::to_string(plan.post[k]) + "," +
@@ -311,7 +306,7 @@ Status solve_graph(decmg_gpu_ctx* c, Driver& dr, const Plan& plan, int nrhs, uns
             cudaGraphConditionalHandle hif;
             DG_CUDA(cudaGraphConditionalHandleCreate(&hif, cg, 0, cudaGraphCondAssignDefault));
             DG_TRY(launch(c, kNorms, 0.0, [&] {
-                k_solve_check<<<1, 32, 0, c->stream>>>(nrhs, dres, gst, c->hist_dev, hif, hw);
+                k_solve_check<<<1, 32, 0, c->stream>>>(nrhs, dres, gst, c->hist_dev, c->tstamp_dev, hif, hw);
             }));
             DG_TRY(launch(c, kNorms, 16.0 * static_cast<double>(total), [&] {
                 k_copy_lanes_dev<<<grid_for(total, kBlock), kBlock, 0, c->stream>>>(total, nrhs, gst, xprev,
@@ -395,6 +390,25 @@ Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, co
              double* h_final, bool staged, const double* bsrc) {
     DG_TRY(check_nrhs(c, nrhs));
     if (max_cycles < 0) return Status::Err(DECMG_INVALID_ARGUMENT, "gmg_solve: max_cycles >= 0");
+    const auto t_host0 = std::chrono::steady_clock::now();
+    c->last_times.clear();
+    if (max_cycles > c->hist_cap) {
+        if (c->hist_dev) cudaFree(c->hist_dev);
+        if (c->tstamp_dev) cudaFree(c->tstamp_dev);
+        c->hist_dev = nullptr;
+        c->tstamp_dev = nullptr;
+        c->hist_cap = 0;
+        DG_CUDA(cudaMalloc(&c->hist_dev, sizeof(double) * max_cycles * 32));
+        DG_CUDA(cudaMalloc(&c->tstamp_dev, sizeof(unsigned long long) * (max_cycles + 1)));
+        c->hist_cap = max_cycles;
+    }
+    if (!c->tstamp_dev) DG_CUDA(cudaMalloc(&c->tstamp_dev, sizeof(unsigned long long) * 1));
+    // device clock at the start (cumulative_seconds of the graph-driven cycles)
+    DG_TRY(launch(c, kNorms, 0.0, [&] { k_stamp<<<1, 1, 0, c->stream>>>(c->tstamp_dev); }));
+    const double t_launch0 = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_host0).count();
+    auto host_elapsed = [&]() {
+        return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_host0).count();
+    };
     Level& L0 = c->lv[0];
     if (!bsrc) bsrc = c->bproj;
     if (!staged) {  // staged: stage_rhs already left the projected RHS in bsrc
@@ -432,8 +446,9 @@ Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, co
             if (h_hist) h_hist[static_cast<int64_t>(cyc - 1) * nrhs + l] = res;
             final_res[l] = res;
             done[l] = cyc;
-            if (res <= tol || cyc == max_cycles) fin |= 1u << l;
+            if (res <= tol || cyc == max_cycles || !std::isfinite(res)) fin |= 1u << l;
         }
+        if (cyc >= 1) c->last_times.push_back(host_elapsed());
         if (fin) {
             DG_TRY(launch(c, kNorms, 16.0 * L0.nv * nrhs, [&] {
                 k_copy_lanes<<<grid_for(total, kBlock), kBlock, 0, c->stream>>>(total, nrhs, fin, xsrc, c->xsol);
@@ -452,10 +467,17 @@ Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, co
         if (on_device) {
             SolveState st;
             std::vector<double> hist(static_cast<size_t>(max_cycles) * nrhs);
+            std::vector<unsigned long long> ts(static_cast<size_t>(max_cycles) + 1);
             DG_CUDA(cudaMemcpyAsync(&st, c->gstate_raw, sizeof(SolveState), cudaMemcpyDeviceToHost, c->stream));
             DG_CUDA(cudaMemcpyAsync(hist.data(), c->hist_dev, sizeof(double) * hist.size(), cudaMemcpyDeviceToHost,
                                     c->stream));
+            DG_CUDA(cudaMemcpyAsync(ts.data(), c->tstamp_dev, sizeof(unsigned long long) * ts.size(),
+                                    cudaMemcpyDeviceToHost, c->stream));
             DG_CUDA(cudaStreamSynchronize(c->stream));
+            int maxdone = 0;
+            for (int l = 0; l < nrhs; ++l) maxdone = std::max(maxdone, st.done[l]);
+            for (int k = 1; k <= maxdone; ++k)  // device clock of each check, offset by the host's launch delay
+                c->last_times.push_back(t_launch0 + 1e-9 * static_cast<double>(ts[k] - ts[0]));
             for (int l = 0; l < nrhs; ++l) {
                 done[l] = st.done[l];
                 final_res[l] = st.final_res[l];
@@ -510,6 +532,12 @@ Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, co
         if (cycles_done) cycles_done[l] = done[l];
         if (h_final) h_final[l] = final_res[l];
     }
+    // NaN/Inf guard on the per-cycle residual: the lane stopped at
+    // the first non-finite residual instead of cycling on to max_cycles
+    for (int l = 0; l < nrhs; ++l)
+        if (!std::isfinite(final_res[l]))
+            return Status::Err(DECMG_RUNTIME, "gmg_solve: non-finite residual (right-hand side " + std::to_string(l) +
+                                                  ", cycle " + std::to_string(done[l]) + ")");
     return Status::Ok();
 }
 
@@ -581,6 +609,54 @@ Status solve_batches(decmg_gpu_ctx* c, const Plan& plan, int nrhs, int nbatch, c
     DG_CUDA(cudaStreamSynchronize(c->d2h_stream));
     DG_CUDA(cudaStreamSynchronize(c->aux_stream));
     return Status::Ok();
+}
+
+// smooth (multigrid.hpp:66-68, multigrid.cpp:95-120) on level k's operator:
+// x = d_x (reference numbering) -> iters sweeps -> d_out. weighted: the CG
+// smoother's inner product uses the level's dual areas (what cycle_once
+// passes); otherwise plain dots (smooth's default `weights = {}`).
+Status smooth_level(decmg_gpu_ctx* c, int k, const Plan& plan, int iters, int nrhs, const double* d_x,
+                    const double* d_b, double* d_out, bool weighted) {
+    DG_TRY(check_nrhs(c, nrhs));
+    const int L = static_cast<int>(c->lv.size());
+    if (k < 0 || k >= L) return Status::Err(DECMG_INVALID_ARGUMENT, "smooth: level out of range");
+    if (iters < 0) return Status::Err(DECMG_INVALID_ARGUMENT, "smooth: negative iteration count");
+    Level& m = c->lv[k];
+    if ((plan.smoother == DECMG_SMOOTHER_GS || plan.smoother == DECMG_SMOOTHER_SGS) && !m.gsf_rows)
+        DG_TRY(build_gs_schedule(c, m));  // the coarsest level has none until asked
+    Driver dr{c, nrhs, bp_of(nrhs), c->lv[0].b};
+    dr.init();
+    const int64_t t = static_cast<int64_t>(m.nv) * nrhs;
+    auto perm = [&](const double* src, double* dst, bool scatter) -> Status {
+        if (!m.ord) {
+            DG_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * t, cudaMemcpyDeviceToDevice, c->stream));
+            return Status::Ok();
+        }
+        return launch(c, kNorms, 16.0 * t, [&] {
+            if (scatter)
+                k_permute<true><<<grid_for(t, kBlock), kBlock, 0, c->stream>>>(m.nv, nrhs, m.ord, src, dst);
+            else
+                k_permute<false><<<grid_for(t, kBlock), kBlock, 0, c->stream>>>(m.nv, nrhs, m.ord, src, dst);
+        });
+    };
+    DG_TRY(perm(d_b, m.b, false));
+    DG_TRY(perm(d_x, m.x[m.cur], false));
+    m.x_zero = false;
+    double* ones = nullptr;
+    if (plan.smoother == DECMG_SMOOTHER_CG && !weighted) {
+        DG_CUDA(cudaMalloc(&ones, sizeof(double) * m.nv));
+        DG_TRY(launch(c, kNorms, 8.0 * m.nv, [&] {
+            k_fill<<<grid_for(m.nv, kBlock), kBlock, 0, c->stream>>>(m.nv, 1.0, ones);
+        }));
+        dr.cg_weights = ones;
+    }
+    Status s = dr.smooth(k, iters, plan);
+    if (s.ok()) s = perm(m.x[m.cur], d_out, true);
+    if (ones) {
+        cudaStreamSynchronize(c->stream);
+        cudaFree(ones);
+    }
+    return s;
 }
 
 Status apply_op(decmg_gpu_ctx* c, int level, char op, const double* d_x, double* d_y) {

@@ -1356,7 +1356,8 @@ Status dist_run(decmg_gpu_dist* D, const Plan& plan, int nrhs, const double* h_b
     }
     for (int l = 0; l < nrhs; ++l)
         if (!std::isfinite(hs.final_res[l]))
-            return Status::Err(DECMG_RUNTIME, "gmg_solve: residual is not finite");
+            return Status::Err(DECMG_RUNTIME, "gmg_solve: non-finite residual (right-hand side " + std::to_string(l) +
+                                                  ", cycle " + std::to_string(hs.done[l]) + ")");
     return Status::Ok();
 }
 

@@ -29,6 +29,7 @@ struct Driver {
     const double* fuse_denom = nullptr;
     std::function<Status(const double*, bool*)> fuse_hook;
     bool stopped = false;
+    const double* cg_weights = nullptr;  // CG smoother inner-product weights (nullptr: the level's dual areas)
 
     void init() {
         const bool vec = nrhs == bp && bp >= 2;
@@ -160,7 +161,7 @@ struct Driver {
         int* done = reinterpret_cast<int*>(c->cgs_s + 160);
         double* x = xcur(L);
         const double* b = bptr(k);
-        const double* w = L.area_i;
+        const double* w = cg_weights ? cg_weights : L.area_i;
         const int cls = k == 0 ? kFineSweep : kCoarseLevels;
         const unsigned g = rows_grid(n);
         const double mbytes = 12.0 * L.nnzL + 4.0 * (n + 1) + 16.0 * n * nrhs;

@@ -13,6 +13,8 @@
 // Vectors live in the internal numbering (common.cuh Level::ord).
 #include "driver.cuh"
 
+#include <chrono>
+
 #include <cmath>
 #include <string>
 #include <vector>
@@ -22,6 +24,11 @@ namespace decmg_gpu {
 Status pcg(decmg_gpu_ctx* c, const Plan& inner, int inner_cycles, int nrhs, const double* d_b, double tol,
            int maxiter, double* d_x, double* h_hist, int* iters, int* converged, double* h_final, bool staged) {
     DG_TRY(check_nrhs(c, nrhs));
+    const auto t_host0 = std::chrono::steady_clock::now();
+    auto host_elapsed = [&]() {
+        return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_host0).count();
+    };
+    c->last_times.clear();
     if (c->dirichlet)
         return Status::Err(DECMG_INVALID_ARGUMENT, "gmg_pcg: Neumann hierarchies only (the reference projects b)");
     if (maxiter < 0) return Status::Err(DECMG_INVALID_ARGUMENT, "gmg_pcg: maxiter >= 0");
@@ -111,6 +118,7 @@ Status pcg(decmg_gpu_ctx* c, const Plan& inner, int inner_cycles, int nrhs, cons
     double* guard = res + 32;  // [kind, iteration] of the first breakdown (pcg_s + 224)
     DG_CUDA(cudaMemsetAsync(guard, 0, sizeof(double) * 2, st));
     DG_TRY(fetch(res, hres));
+    c->last_times.push_back(host_elapsed());  // weighted_cg records the initial residual's time too
     unsigned active = 0;
     for (int l = 0; l < nrhs; ++l) {
         if (h_hist) h_hist[l] = hres[l];
@@ -145,6 +153,7 @@ Status pcg(decmg_gpu_ctx* c, const Plan& inner, int inner_cycles, int nrhs, cons
                                                                            : "cg: breakdown (non-finite step)") +
                                                   " at iteration " + std::to_string(static_cast<int>(hres_g[33])));
         for (int l = 0; l < nrhs; ++l) hres[l] = hres_g[l];
+        c->last_times.push_back(host_elapsed());
         for (int l = 0; l < nrhs; ++l) {
             if (!(active & (1u << l))) continue;
             if (h_hist) h_hist[static_cast<size_t>(it) * nrhs + l] = hres[l];

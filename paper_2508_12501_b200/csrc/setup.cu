@@ -871,7 +871,17 @@ Status mesh_from_triangles(decmg_gpu_ctx* c, Level& m, double* pos, int nv, int*
 }
 
 // build_dual + laplacian_0 + boundary for one level.
-Status assemble(decmg_gpu_ctx* c, Level& m, bool dirichlet) {
+__global__ void k_clamp_area(int nv, double floor_area, double* __restrict__ area) {
+    const int64_t i = gtid();
+    if (i < nv && area[i] <= 0.0) area[i] = floor_area;
+}
+// dual_areas = 1 / star0_inv (operators.cpp:109-114, clamped assembly)
+__global__ void k_area_from_inv(int nv, double* __restrict__ area) {
+    const int64_t i = gtid();
+    if (i < nv) area[i] = __ddiv_rn(1.0, __ddiv_rn(1.0, area[i]));
+}
+
+Status assemble(decmg_gpu_ctx* c, Level& m, bool dirichlet, bool clamp) {
     TmpPool tp(c->stream);
     const int nv = m.nv, ne = m.ne, nt = m.nt;
     int *bad_edge, *bad_tri, *bad_area, *zero_diag;
@@ -899,6 +909,17 @@ Status assemble(decmg_gpu_ctx* c, Level& m, bool dirichlet) {
     LAUNCH(4, ne, k_edge_w, ne, et_ptr, et, dist, plen, w);
     DG_TRY(dalloc(c, &m.area, nv));
     LAUNCH(4, nv, k_vertex_area, nv, vt_ptr, vt, wedge, m.area);
+    if (clamp) {
+        // HodgeOptions::clamp_dual_areas (operators.cpp:80-98): nonpositive areas
+        // become 1e-14 * mean, the mean summed in vertex order
+        std::vector<double> a(nv);
+        DG_CUDA(cudaMemcpyAsync(a.data(), m.area, sizeof(double) * nv, cudaMemcpyDeviceToHost, c->stream));
+        DG_CUDA(cudaStreamSynchronize(c->stream));
+        double mean = 0.0;
+        for (double x : a) mean += x;
+        mean /= std::max(nv, 1);
+        LAUNCH(4, nv, k_clamp_area, nv, 1e-14 * mean, m.area);
+    }
     DG_TRY(dalloc(c, &m.bd, nv));
     DG_CUDA(cudaMemsetAsync(m.bd, 0, nv * sizeof(int), c->stream));
     LAUNCH(4, ne, k_boundary, ne, et_ptr, m.edges, m.bd);
@@ -915,6 +936,7 @@ Status assemble(decmg_gpu_ctx* c, Level& m, bool dirichlet) {
     LAUNCH(4, nv, k_lap_fill, nv, m.edges, m.ve_ptr, m.ve, w, m.area, m.bd, dirichlet ? 1 : 0,
            m.L_rp, m.L_ci, m.L_v, m.diag, bad_area, zero_diag);
     DG_TRY(check_flag(c, bad_area, "hodge_star_0_inv: non-well-centered dual cell at vertex"));
+    if (clamp) LAUNCH(4, nv, k_area_from_inv, nv, m.area);
     int zd = 0;
     DG_TRY(read_int(c, zero_diag, &zd));
     m.zero_diag_row = zd == 0x7fffffff ? -1 : zd;
@@ -1034,6 +1056,8 @@ Status build_ell(decmg_gpu_ctx* c, int nrows, const int* rp, const int* ci, cons
 
 // Phases of the exact Gauss-Seidel sweeps (both directions) and their
 // internal row lists, ascending within a phase (stable radix sort by phase).
+}  // namespace
+
 Status build_gs_schedule(decmg_gpu_ctx* c, Level& m) {
     TmpPool tp(c->stream);
     const int n = m.nv;
@@ -1078,6 +1102,8 @@ Status build_gs_schedule(decmg_gpu_ctx* c, Level& m) {
     }
     return Status::Ok();
 }
+
+namespace {
 
 // Internal numbering for every level except the coarsest (its CG runs
 // sequentially in the reference order): Morton order, the renumbered L, P, R
@@ -1148,9 +1174,10 @@ Status exclusive_scan(decmg_gpu_ctx* c, const int* in, int* out, int n) {
 }
 
 Status build_from_base(decmg_gpu_ctx* c, const double* hpos, int nv, const int* hcorners, int nt,
-                       int nsub, unsigned flags) {
+                       int nsub, unsigned flags, int use_levels) {
     if (nv < 3 || nt < 1 || nsub < 0) return Status::Err(DECMG_INVALID_ARGUMENT, "create_from_base: bad sizes");
-    const int L = nsub + 1;
+    if (use_levels < 0) return Status::Err(DECMG_INVALID_ARGUMENT, "create_from_base: use_levels >= 0");
+    int L = nsub + 1;
     const bool cubic = (flags & DECMG_CUBIC) != 0;
     // size guard: every count must stay inside int32 (reference uses int)
     {
@@ -1195,7 +1222,13 @@ Status build_from_base(decmg_gpu_ctx* c, const double* hpos, int nv, const int* 
         }
         DG_TRY(mesh_from_triangles(c, c->lv[k], fpos, fnv, fcor, fnt));
     }
-    for (int k = 0; k < L; ++k) DG_TRY(assemble(c, c->lv[k], c->dirichlet));
+    // build_hierarchy's use_levels (multigrid.cpp:333-337): keep the finest
+    // use_levels meshes; the coarse solve then runs on a finer mesh
+    if (use_levels > 0 && use_levels < L) {
+        L = use_levels;
+        c->lv.resize(L);
+    }
+    for (int k = 0; k < L; ++k) DG_TRY(assemble(c, c->lv[k], c->dirichlet, (flags & DECMG_CLAMP_DUAL_AREAS) != 0));
     for (int k = 0; k + 1 < L; ++k) {
         Level& f = c->lv[k];
         const Level& cm = c->lv[k + 1];

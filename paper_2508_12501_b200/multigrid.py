@@ -229,12 +229,15 @@ class MultigridHierarchy:
     # -- construction ------------------------------------------------------
     @classmethod
     def from_base(cls, base, nsub: int, dirichlet: bool = False, project_sphere: Optional[bool] = None,
-                  device: int = 0, max_nrhs: int = 1, cubic: bool = False) -> "MultigridHierarchy":
-        """build_hierarchy(base, subdivision_tower(base, Binary|Cubic, nsub)) on the GPU.
+                  device: int = 0, max_nrhs: int = 1, cubic: bool = False, use_levels: int = 0,
+                  clamp_dual_areas: bool = False) -> "MultigridHierarchy":
+        """build_hierarchy(base, subdivision_tower(base, Binary|Cubic, nsub), use_levels,
+        HierarchyOptions{hodge.clamp_dual_areas}) on the GPU (multigrid.cpp:325-341).
 
         base: a spec string for base_mesh() -- with the suffix "+cubic" for
         SubdivisionScheme::Cubic, as in the reference harness -- or a
-        (positions, corner_triples) pair.
+        (positions, corner_triples) pair. use_levels > 0 keeps only the finest
+        use_levels meshes (the coarse solve runs on a finer mesh).
         """
         lib = _lib.load()
         if isinstance(base, str):
@@ -249,11 +252,11 @@ class MultigridHierarchy:
         pos = np.ascontiguousarray(pos, dtype=np.float64)
         tri = np.ascontiguousarray(tri, dtype=np.int32)
         flags = ((_lib.DECMG_PROJECT_SPHERE if project_sphere else 0) | (_lib.DECMG_DIRICHLET if dirichlet else 0)
-                 | (_lib.DECMG_CUBIC if cubic else 0))
+                 | (_lib.DECMG_CUBIC if cubic else 0) | (_lib.DECMG_CLAMP_DUAL_AREAS if clamp_dual_areas else 0))
         cfg = decmg_gpu_config(device=device, max_nrhs=max_nrhs)
         out = C.c_void_p()
-        check(lib.decmg_gpu_create_from_base(_ptr(pos), pos.shape[0], _ptr(tri), tri.shape[0], nsub, flags,
-                                             C.byref(cfg), C.byref(out)))
+        check(lib.decmg_gpu_create_from_base_ex(_ptr(pos), pos.shape[0], _ptr(tri), tri.shape[0], nsub, use_levels,
+                                                flags, C.byref(cfg), C.byref(out)))
         return cls(out.value, dirichlet, max_nrhs)
 
     @classmethod
@@ -424,6 +427,32 @@ class MultigridHierarchy:
         return self._lib.decmg_gpu_stream(self._ctx)
 
 
+def _last_times(h) -> list:
+    """SolveReport::cumulative_seconds of the last solve / pcg on h (decmg_gpu_last_times)."""
+    n = h._lib.decmg_gpu_last_times(h.ctx, None, 0)
+    t = np.zeros(max(n, 0))
+    if n > 0:
+        h._lib.decmg_gpu_last_times(h.ctx, _ptr(t), n)
+    return t.tolist()
+
+
+def smooth(h: "MultigridHierarchy", k: int, x: np.ndarray, b: np.ndarray, cfg: "SmootherConfig", iters: int,
+           weighted: bool = False) -> np.ndarray:
+    """smooth(A = level k's Laplacian, x, b, cfg, iters, weights) (multigrid.hpp:66-68,
+    multigrid.cpp:95-120) on the device; returns the smoothed x. weighted: the CG
+    smoother's inner product uses the level's dual areas (cycle_once's call),
+    else plain dots (the reference's default weights = {})."""
+    n = h.level_info(k)["nv"]
+    xx = np.array(x, dtype=np.float64, copy=True, order="C")
+    bb = np.ascontiguousarray(b, dtype=np.float64)
+    if xx.shape[0] != n or bb.shape != xx.shape:
+        raise ValueError("smooth: shape mismatch")
+    nrhs = 1 if xx.ndim == 1 else xx.shape[1]
+    check(h._lib.decmg_gpu_smooth(h.ctx, k, _SMOOTHER_C[cfg.method], cfg.jacobi_omega, iters, nrhs, _ptr(xx),
+                                  _ptr(bb), int(weighted)), h.ctx)
+    return xx
+
+
 def build_hierarchy(base, nsub: int, **kw) -> MultigridHierarchy:
     """build_hierarchy(base, subdivision_tower(base, Binary, nsub)) (multigrid.cpp:325-341)."""
     return MultigridHierarchy.from_base(base, nsub, **kw)
@@ -445,13 +474,17 @@ def gmg_solve(h: MultigridHierarchy, plan: CyclePlan, b: np.ndarray, tol: float,
     check(h._lib.decmg_gpu_solve(h.ctx, C.byref(ps), nrhs, _ptr(b), None if x0 is None else _ptr(x0), tol,
                                  max_cycles, _ptr(x), _ptr(hist), _ptr(done), _ptr(final)), h.ctx)
     wall = time.perf_counter() - t0
+    times = _last_times(h)
     if b.ndim == 1:
         it = int(done[0])
-        return SolveReport(solution=x, residual_history=hist[:it, 0].tolist(), cumulative_seconds=[],
-                           iterations=it, converged=bool(final[0] <= tol), final_relative_residual=float(final[0]),
-                           wall_seconds=wall)
-    return SolveReport(solution=x, residual_history=[hist[: done[j], j].tolist() for j in range(nrhs)],
-                       cumulative_seconds=[], iterations=done.tolist(), converged=(final <= tol).tolist(),
+        hl = hist[:it, 0].tolist()
+        return SolveReport(solution=x, residual_history=hl, cumulative_seconds=times[:it],
+                           iterations=it, converged=bool((hl[-1] if it else final[0]) <= tol),
+                           final_relative_residual=float(final[0]), wall_seconds=wall)
+    hl = [hist[: done[j], j].tolist() for j in range(nrhs)]
+    return SolveReport(solution=x, residual_history=hl, cumulative_seconds=[times[: done[j]] for j in range(nrhs)],
+                       iterations=done.tolist(),
+                       converged=[bool((hl[j][-1] if done[j] else final[j]) <= tol) for j in range(nrhs)],
                        final_relative_residual=final.tolist(), wall_seconds=wall)
 
 
@@ -516,14 +549,16 @@ def gmg_preconditioned_cg(h: MultigridHierarchy, inner_plan: CyclePlan, b: np.nd
     check(h._lib.decmg_gpu_pcg(h.ctx, C.byref(ps), int(inner_plan.cycles), nrhs, _ptr(b), tol, maxiter, _ptr(x),
                                _ptr(hist), _ptr(its), _ptr(conv), _ptr(final)), h.ctx)
     wall = time.perf_counter() - t0
+    times = _last_times(h)
     if b.ndim == 1:
         it = int(its[0])
-        return SolveReport(solution=x, residual_history=hist[: it + 1, 0].tolist(), cumulative_seconds=[],
+        return SolveReport(solution=x, residual_history=hist[: it + 1, 0].tolist(), cumulative_seconds=times[: it + 1],
                            iterations=it, converged=bool(conv[0]), final_relative_residual=float(final[0]),
-                           wall_seconds=wall)
+                           wall_seconds=wall, config_echo={"solver": "gmg_pcg"})
     return SolveReport(solution=x, residual_history=[hist[: its[j] + 1, j].tolist() for j in range(nrhs)],
-                       cumulative_seconds=[], iterations=its.tolist(), converged=[bool(v) for v in conv],
-                       final_relative_residual=final.tolist(), wall_seconds=wall)
+                       cumulative_seconds=[times[: its[j] + 1] for j in range(nrhs)], iterations=its.tolist(),
+                       converged=[bool(v) for v in conv], final_relative_residual=final.tolist(), wall_seconds=wall,
+                       config_echo={"solver": "gmg_pcg"})
 
 
 class DistributedHierarchy:

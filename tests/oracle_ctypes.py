@@ -53,6 +53,7 @@ def lib() -> C.CDLL:
                                 C.c_double, C.c_int, C.c_void_p, C.c_void_p,
                                 C.POINTER(C.c_int), C.POINTER(C.c_double)]
         L.orc_coarse_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_smooth.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_void_p, C.c_void_p]
         L.orc_pcg.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                               C.c_void_p, C.c_double, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         _lib = L
@@ -162,6 +163,14 @@ class OracleHierarchy:
         if rc:
             raise RuntimeError(lib().orc_last_error().decode())
         return x, hist[: it.value + 1], it.value, fin.value
+
+    def smooth(self, k, b, x, iters, smoother=1, omega=2.0 / 3.0):
+        """smooth (multigrid.cpp:95-120) on level k's Laplacian; returns the new x."""
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.array(x, dtype=np.float64, copy=True)
+        if lib().orc_smooth(self.h, k, smoother, omega, iters, _p(b), _p(x)):
+            raise RuntimeError(lib().orc_last_error().decode())
+        return x
 
     def coarse_solve(self, b):
         b = np.ascontiguousarray(b, dtype=np.float64)
