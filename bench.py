@@ -456,39 +456,72 @@ def run_partitioned(args, world, rank, local):
 
 
 # ------------------------------------------------------------- reference ----
+def host_cpu():
+    """nproc / lscpu of the host the reference arm runs on."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core", "CPU(s)",
+                             "NUMA node(s)"):
+                info[k.strip()] = v.strip()
+    except Exception:
+        pass
+    return info
+
+
 def run_reference(args, world, rank):
     """The reference's own CPU solver (oracle/_ref/ref_harness: the reference
-    library compiled in place + stand-in coarse solve), all host threads."""
+    library compiled in place + stand-in coarse solve) on all host threads.
+
+    N = 1: the headline workload's mesh (BASELINE config 4, icosphere x10),
+    per-unknown rate of one RHS (the reference has no batched solve: a
+    16-RHS batch is 16 solves one after another at this rate), so
+    config.workload matches our arm. N > 1: our arm runs config 5b
+    (icosphere x11), whose reference setup (std::set/std::map mesh
+    construction, ~50 GB) does not fit the run's time; the sample is the same
+    icosphere family at x10 and says so."""
     if rank != 0:
         return
     harness = ROOT / "oracle" / "_ref" / "ref_harness"
     cores = os.cpu_count() or 1
     env = dict(os.environ, OMP_NUM_THREADS=str(cores), OMP_PROC_BIND="close", OMP_PLACES="cores")
+    nsub = args.ref_nsub if args.ref_nsub else NSUB
+    steps = max(args.steps, 1)
     if harness.exists():
         kind = "reference"
-        # bounded sample: the reference's setup at 10.5 M vertices takes minutes
-        # (std::set/std::map mesh construction), so the sample mesh is the same
-        # family one level coarser unless --ref-nsub says otherwise.
-        nsub = args.ref_nsub
-        cmd = [str(harness), "time", "ico", str(nsub), "neumann", "1", str(max(args.steps, 1)), "1e-8", "0"]
+        cmd = [str(harness), "time", "ico", str(nsub), "neumann", "1", str(steps), "1e-8", "0"]
         res = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=3600)
         if res.returncode != 0:
             print(json.dumps({"impl": "reference", "unavailable": res.stderr.strip()[-200:]}))
             return
         r = json.loads(res.stdout)
         value = r["unknown_cycles_per_s"]
-        sample = (f"reference run_cycle (t(2K)-t(K))/K protocol, K={max(args.steps, 1)}, 1 RHS, icosphere x{nsub} "
-                  f"({r['n']} vertices; reference setup {r['setup_s']:.1f} s), {r['threads']} OpenMP threads")
         n = r["n"]
+        sample = (f"reference run_cycle, (t(2K)-t(K))/K protocol (decmg_main.cpp:133-147), K={steps}, 1 RHS, "
+                  f"icosphere x{nsub} ({n} vertices; reference setup {r['setup_s']:.1f} s untimed), "
+                  f"{r['threads']} OpenMP threads")
+        cores = r["threads"]
     else:
         kind = "port"
         cb = cpu_baseline_port()
         value, sample, n = cb["value"], cb["sample"], None
         cores = 1
+    if world == 1 and nsub == NSUB:
+        levels = nsub + 1
+        workload = (f"BASELINE config 4: icosphere x{nsub} ({n} vertices, {levels} levels), {args.nrhs} RHS batch, "
+                    f"weighted-Jacobi V(2,2), coarse CG, fp64")
+        config = {"workload": workload, "vertices": n, "levels": levels, "nrhs": args.nrhs,
+                  "reference_batch": "the reference solves one RHS at a time; value = its per-unknown rate",
+                  "host": host_cpu()}
+    else:
+        config = {"workload": f"BASELINE config 5b family (icosphere), reference CPU solver on the x{nsub} sample "
+                              f"(our arm: icosphere x{args.scale_nsub} over {world} GPUs)",
+                  "sample_vertices": n, "host": host_cpu()}
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "dtype": "f64",
-           "data": "synthetic", "config": {"workload": f"BASELINE config 4 family (icosphere), reference CPU solver",
-                                           "sample_vertices": n},
+           "data": "synthetic", "config": config,
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -502,7 +535,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--nsub", type=int, default=NSUB)
     ap.add_argument("--nrhs", type=int, default=NRHS)
-    ap.add_argument("--ref-nsub", type=int, default=9)
+    ap.add_argument("--ref-nsub", type=int, default=0, help="reference arm mesh (default: x10, config 4's mesh)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partitioned", action="store_true",
                     help="print the config-5b partitioned line at N = 1 instead of the config-4 headline")

@@ -305,13 +305,18 @@ public:
         }
         meshes_ = meshes;
         decmg_gpu_ctx* c = nullptr;
-        if (!opts.galerkin && !opts.hodge.clamp_dual_areas) c = try_device_tower(meshes, device, max_nrhs);
+        if (!opts.galerkin)
+            c = try_device_tower(meshes, opts.hodge.clamp_dual_areas ? DECMG_CLAMP_DUAL_AREAS : 0u, device, max_nrhs);
+        on_device_ = c != nullptr;
         if (!c) c = assemble_on_host(meshes, maps, opts, device, max_nrhs);
         adopt(c);
     }
 #endif
 
     int levels() const { return decmg_gpu_levels(ctx_.get()); }
+    /// true: meshes and operators were built on the device (subdivision tower
+    /// recognised); false: assembled on the host by the reference and uploaded
+    bool assembled_on_device() const { return on_device_; }
     int fine_rows() const {
         int64_t c[6];
         detail::check(decmg_gpu_level_info(ctx_.get(), 0, c), ctx_.get());
@@ -402,7 +407,7 @@ private:
     }
     // The device tower of the coarsest mesh, if it reproduces every given mesh.
     static decmg_gpu_ctx* try_device_tower(const std::vector<std::shared_ptr<const EmbeddedComplex2D>>& meshes,
-                                           int device, int max_nrhs) {
+                                           unsigned hodge, int device, int max_nrhs) {
         const int L = static_cast<int>(meshes.size());
         std::vector<double> pos;
         std::vector<int> tri;
@@ -420,14 +425,16 @@ private:
         for (unsigned proj : {0u, static_cast<unsigned>(DECMG_PROJECT_SPHERE)}) {
             decmg_gpu_ctx* c = nullptr;
             if (L >= 2) {
-                if (decmg_gpu_create_from_base(pos.data(), V, tri.data(), T, 1, scheme | proj, &cfg, &c) != DECMG_OK)
+                if (decmg_gpu_create_from_base(pos.data(), V, tri.data(), T, 1, scheme | proj | hodge, &cfg, &c) !=
+                    DECMG_OK)
                     return nullptr;
                 const bool ok = hashes_match(c, meshes, L - 2);
                 decmg_gpu_destroy(c);
                 c = nullptr;
                 if (!ok) continue;
             }
-            if (decmg_gpu_create_from_base(pos.data(), V, tri.data(), T, L - 1, scheme | proj, &cfg, &c) != DECMG_OK)
+            if (decmg_gpu_create_from_base(pos.data(), V, tri.data(), T, L - 1, scheme | proj | hodge, &cfg, &c) !=
+                DECMG_OK)
                 return nullptr;
             if (hashes_match(c, meshes, 0)) return c;
             decmg_gpu_destroy(c);
@@ -489,6 +496,7 @@ private:
 #endif
     std::shared_ptr<decmg_gpu_ctx> ctx_{nullptr, Del{}};
     std::vector<MultigridLevel> levels_;
+    bool on_device_ = true;
 };
 
 #ifdef DECMG_GPU_REFERENCE_TYPES

@@ -783,6 +783,32 @@ void orc_project(const orc_hier* h, double* b) {
     for (int i = 0; i < lv->m.nv; ++i) b[i] -= mean;
 }
 
+/* The stand-in's sums: n <= 32 terms are added in index
+ * order from 0.0; longer sums use a fixed-shape tree -- chunks of 256
+ * consecutive terms, zero-padded, folded pairwise (s[t] += s[t + h] for
+ * h = 128, 64, ..., 1), then the chunk sums the same way until one is left --
+ * which the device's grid CG reproduces (rowkernels.cuh k_coarse_cg_grid).
+ * q is overwritten. */
+static double standin_sum(double* q, int64_t n) {
+    if (n <= 32) {
+        double s = 0.0;
+        for (int64_t i = 0; i < n; ++i) s += q[i];
+        return s;
+    }
+    while (n > 1) {
+        const int64_t nc = (n + 255) / 256;
+        for (int64_t c = 0; c < nc; ++c) {
+            double t[256];
+            for (int j = 0; j < 256; ++j) t[j] = c * 256 + j < n ? q[c * 256 + j] : 0.0;
+            for (int h = 128; h >= 1; h >>= 1)
+                for (int j = 0; j < h; ++j) t[j] = t[j] + t[j + h];
+            q[c] = t[0];
+        }
+        n = nc;
+    }
+    return q[0];
+}
+
 /* Coarse solve: projected weighted CG (oracle/ref_standin_direct.cpp, the
  * stand-in for PinnedDirectSolver::solve, proj/src/direct.cpp:59-76).
  * Dirichlet (x1): same CG without the two projections. */
@@ -793,40 +819,39 @@ static void coarse_cg(const level_t* lv, double wtot, int project, const double*
     double* r = NEW(double, n);
     double* p = NEW(double, n);
     double* Ap = NEW(double, n);
+    double* q = NEW(double, n);
     memcpy(rhs, b, (size_t)n * sizeof(double));
     if (project) {
-        double m = 0.0;
-        for (int i = 0; i < n; ++i) m += w[i] * b[i];
-        m = m / wtot;
+        for (int i = 0; i < n; ++i) q[i] = w[i] * b[i];
+        const double m = standin_sum(q, n) / wtot;
         for (int i = 0; i < n; ++i) rhs[i] = b[i] - m;
     }
     for (int i = 0; i < n; ++i) { x[i] = 0.0; r[i] = rhs[i]; p[i] = rhs[i]; }
-    double rr = 0.0;
-    for (int i = 0; i < n; ++i) rr += (w[i] * r[i]) * r[i];
+    for (int i = 0; i < n; ++i) q[i] = (w[i] * r[i]) * r[i];
+    double rr = standin_sum(q, n);
     const double rr0 = rr;
     const int maxit = 4 * n + 20;
     for (int it = 0; it < maxit; ++it) {
         if (!(rr > 1e-30 * rr0)) break;
         csr_apply(n, lv->L_rp, lv->L_ci, lv->L_v, p, Ap);
-        double curv = 0.0;
-        for (int i = 0; i < n; ++i) curv += (w[i] * p[i]) * Ap[i];
+        for (int i = 0; i < n; ++i) q[i] = (w[i] * p[i]) * Ap[i];
+        const double curv = standin_sum(q, n);
         if (curv == 0.0) break;
         const double alpha = rr / curv;
         for (int i = 0; i < n; ++i) x[i] = x[i] + alpha * p[i];
         for (int i = 0; i < n; ++i) r[i] = r[i] - alpha * Ap[i];
-        double rn = 0.0;
-        for (int i = 0; i < n; ++i) rn += (w[i] * r[i]) * r[i];
+        for (int i = 0; i < n; ++i) q[i] = (w[i] * r[i]) * r[i];
+        const double rn = standin_sum(q, n);
         const double beta = rn / rr;
         for (int i = 0; i < n; ++i) p[i] = r[i] + beta * p[i];
         rr = rn;
     }
     if (project) {
-        double ym = 0.0;
-        for (int i = 0; i < n; ++i) ym += w[i] * x[i];
-        ym = ym / wtot;
+        for (int i = 0; i < n; ++i) q[i] = w[i] * x[i];
+        const double ym = standin_sum(q, n) / wtot;
         for (int i = 0; i < n; ++i) x[i] = x[i] - ym;
     }
-    free(rhs); free(r); free(p); free(Ap);
+    free(rhs); free(r); free(p); free(Ap); free(q);
 }
 
 void orc_coarse_solve(const orc_hier* h, const double* b, double* x) {

@@ -27,6 +27,8 @@
 
 #include <omp.h>
 
+#include "ref_cases.hpp"
+
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -43,6 +45,11 @@ std::vector<double> standin_coarse_cg(const SparseOperator& A, const std::vector
 }
 
 using namespace decmg;
+using refcases::Case;
+using refcases::ico_base;
+using refcases::make_case;
+using refcases::projected_subdivide;
+using refcases::tower_of;
 
 namespace {
 
@@ -64,99 +71,7 @@ std::uint64_t fnv_vec(const std::vector<T>& v) {
     return fnv(v.data(), v.size() * sizeof(T));
 }
 
-// ---- extension x2: canonical icosahedron ------------------------
-std::shared_ptr<EmbeddedComplex2D> ico_base() {
-    const double phi = (1.0 + std::sqrt(5.0)) / 2.0;
-    const double raw[12][3] = {{-1, phi, 0}, {1, phi, 0},  {-1, -phi, 0}, {1, -phi, 0},
-                               {0, -1, phi}, {0, 1, phi},  {0, -1, -phi}, {0, 1, -phi},
-                               {phi, 0, -1}, {phi, 0, 1},  {-phi, 0, -1}, {-phi, 0, 1}};
-    std::vector<Vec3> pos;
-    for (const auto& r : raw) {
-        Vec3 p(r[0], r[1], r[2]);
-        const double s = 1.0 / p.norm();
-        pos.push_back(p * s);
-    }
-    const std::vector<std::array<int, 3>> tris = {
-        {0, 11, 5}, {0, 5, 1},  {0, 1, 7},   {0, 7, 10}, {0, 10, 11},
-        {1, 5, 9},  {5, 11, 4}, {11, 10, 2}, {10, 7, 6}, {7, 1, 8},
-        {3, 9, 4},  {3, 4, 2},  {3, 2, 6},   {3, 6, 8},  {3, 8, 9},
-        {4, 9, 5},  {2, 4, 11}, {6, 2, 10},  {8, 6, 7},  {9, 8, 1}};
-    return EmbeddedComplex2D::from_triangles(std::move(pos), tris);
-}
-
-// Projected subdivision: the reference's binary (or cubic) subdivide, then
-// every new vertex is pushed to the unit sphere as p * (1.0 / |p|); copied
-// vertices keep their bits. Map columns are unchanged.
-SubdivisionResult projected_subdivide(const std::shared_ptr<const EmbeddedComplex2D>& c, bool cubic = false) {
-    SubdivisionResult s = cubic ? cubic_subdivide(c) : binary_subdivide(c);
-    const int nvc = c->num_vertices();
-    std::vector<Vec3> pos = s.fine->positions;
-    for (std::size_t v = nvc; v < pos.size(); ++v) {
-        const double inv = 1.0 / pos[v].norm();
-        pos[v] = pos[v] * inv;
-    }
-    std::vector<std::array<int, 3>> tris;
-    tris.reserve(s.fine->num_triangles());
-    for (int t = 0; t < s.fine->num_triangles(); ++t) tris.push_back(s.fine->corners(t));
-    auto fine = EmbeddedComplex2D::from_triangles(std::move(pos), tris);
-    SubdivisionResult out;
-    out.map = GeometricMap::make(fine, c, s.map.columns());
-    out.fine = fine;
-    out.provenance = std::move(s.provenance);
-    return out;
-}
-
-struct Case {
-    std::shared_ptr<EmbeddedComplex2D> base;
-    bool project = false;
-    bool cubic = false;  // SubdivisionScheme::Cubic (1 -> 9) instead of Binary
-};
-
-// <base>[+cubic], base one of square | ico | grid:nx:ny:lx:ly | equi:rows:cols:side
-Case make_case(const std::string& spec_in) {
-    Case c;
-    std::string spec = spec_in;
-    const std::string suffix = "+cubic";
-    if (spec.size() > suffix.size() && spec.compare(spec.size() - suffix.size(), suffix.size(), suffix) == 0) {
-        c.cubic = true;
-        spec = spec.substr(0, spec.size() - suffix.size());
-    }
-    if (spec == "square") {
-        c.base = make_triangulated_grid(1, 1, 1.0, 1.0);
-    } else if (spec == "ico") {
-        c.base = ico_base();
-        c.project = true;
-    } else if (spec.rfind("grid:", 0) == 0) {
-        int nx, ny;
-        double lx, ly;
-        if (std::sscanf(spec.c_str(), "grid:%d:%d:%lf:%lf", &nx, &ny, &lx, &ly) != 4)
-            throw std::invalid_argument("bad grid spec");
-        c.base = make_triangulated_grid(nx, ny, lx, ly);
-    } else if (spec.rfind("equi:", 0) == 0) {
-        int r, cc;
-        double side;
-        if (std::sscanf(spec.c_str(), "equi:%d:%d:%lf", &r, &cc, &side) != 3)
-            throw std::invalid_argument("bad equi spec");
-        c.base = make_equilateral_grid(r, cc, side);
-    } else {
-        throw std::invalid_argument("unknown case " + spec);
-    }
-    return c;
-}
-
-std::vector<SubdivisionResult> tower_of(const Case& c, int k) {
-    if (k == 0) return {};
-    if (!c.project)
-        return subdivision_tower(c.base, c.cubic ? SubdivisionScheme::Cubic : SubdivisionScheme::Binary, k);
-    std::vector<SubdivisionResult> chain;
-    std::shared_ptr<const EmbeddedComplex2D> cur = c.base;
-    for (int i = 0; i < k; ++i) {
-        chain.push_back(projected_subdivide(cur, c.cubic));
-        cur = chain.back().fine;
-    }
-    std::reverse(chain.begin(), chain.end());
-    return chain;
-}
+// ico_base, projected_subdivide, Case, make_case, tower_of: oracle/ref_cases.hpp
 
 // ---- extension x3: RHS generators --------------------------------
 std::vector<double> make_rhs(const std::string& kind, const EmbeddedComplex2D& m,
@@ -424,11 +339,26 @@ int cmd_cycles(const Case& c, int k, bool dirichlet, const std::string& rhs, std
     return 0;
 }
 
+// solve ... [smoother] [use_levels] [rediscretize|galerkin] [V|W|F] [pre] [post]:
+// build_hierarchy(base, tower, use_levels, HierarchyOptions{galerkin})
+// (multigrid.cpp:196-238, 325-341) and standard_plan(levels, kind, pre, post)
+struct SolveOpts {
+    int use_levels = 0;
+    bool galerkin = false;
+    bool clamp = false;  // HodgeOptions::clamp_dual_areas
+    std::string kind = "V";
+    int pre = 2, post = 2;
+};
+
 int cmd_solve(const Case& c, int k, bool dirichlet, const std::string& rhs, std::uint64_t seed,
-              double tol, int maxc, const std::string& smoother) {
+              double tol, int maxc, const std::string& smoother, const SolveOpts& so = {}) {
     const auto tower = tower_of(c, k);
-    MultigridHierarchy h = build_hierarchy(c.base, tower);
-    CyclePlan plan = standard_plan(h.levels(), CycleKind::V, 2, 2, smoother_of(smoother));
+    HierarchyOptions hopts;
+    hopts.galerkin = so.galerkin;
+    hopts.hodge.clamp_dual_areas = so.clamp;
+    MultigridHierarchy h = build_hierarchy(c.base, tower, so.use_levels, hopts);
+    const CycleKind kind = so.kind == "W" ? CycleKind::W : (so.kind == "F" ? CycleKind::F : CycleKind::V);
+    CyclePlan plan = standard_plan(h.levels(), kind, so.pre, so.post, smoother_of(smoother));
     const auto& m = *h.level(0).mesh;
     std::vector<double> hist, x;
     int iters = 0;
@@ -569,7 +499,8 @@ int main(int argc, char** argv) {
             std::fprintf(stderr,
                          "usage: ref_harness structure <case> <k> <bc> [full]\n"
                          "       ref_harness cycles <case> <k> <bc> <rhs> <seed> <ncycles> [jacobi|gs|sgs|cg]\n"
-                         "       ref_harness solve <case> <k> <bc> <rhs> <seed> <tol> <maxc> [jacobi|gs|sgs|cg]\n"
+                         "       ref_harness solve <case> <k> <bc> <rhs> <seed> <tol> <maxc> [jacobi|gs|sgs|cg] "
+                         "[use_levels] [rediscretize|galerkin|clamp|galerkin+clamp] [V|W|F] [pre] [post]\n"
                          "       ref_harness time <case> <k> <bc> <nrhs> <ncyc> <tol> <maxc> [jacobi|gs|sgs|cg]\n"
                          "       ref_harness write <case> <k> <level> <obj|L|P|R> <out>\n"
                          "       ref_harness readobj <file.obj>\n"
@@ -589,9 +520,20 @@ int main(int argc, char** argv) {
         if (cmd == "cycles")
             return cmd_cycles(c, k, dirichlet, argv[5], std::strtoull(argv[6], nullptr, 10),
                               std::atoi(argv[7]), argc > 8 ? argv[8] : "jacobi");
-        if (cmd == "solve")
+        if (cmd == "solve") {
+            SolveOpts so;
+            if (argc > 10) so.use_levels = std::atoi(argv[10]);
+            if (argc > 11) {
+                const std::string o = argv[11];
+                so.galerkin = o.find("galerkin") != std::string::npos;
+                so.clamp = o.find("clamp") != std::string::npos;
+            }
+            if (argc > 12) so.kind = argv[12];
+            if (argc > 13) so.pre = std::atoi(argv[13]);
+            if (argc > 14) so.post = std::atoi(argv[14]);
             return cmd_solve(c, k, dirichlet, argv[5], std::strtoull(argv[6], nullptr, 10),
-                             std::atof(argv[7]), std::atoi(argv[8]), argc > 9 ? argv[9] : "jacobi");
+                             std::atof(argv[7]), std::atoi(argv[8]), argc > 9 ? argv[9] : "jacobi", so);
+        }
         if (cmd == "time")
             return cmd_time(c, k, dirichlet, std::atoi(argv[5]), std::atoi(argv[6]),
                             std::atof(argv[7]), std::atoi(argv[8]), argc > 9 ? argv[9] : "jacobi");

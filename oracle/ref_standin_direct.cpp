@@ -44,19 +44,41 @@ CsrCopy copy_csr(const SparseOperator& A) {
 
 // Projected weighted CG; arithmetic order documented in DESIGN.md and mirrored
 // by dec_coarse_cg (oracle/decmg_oracle.c) and coarse_cg_kernel (CUDA).
+// The stand-in's sums: index order from 0.0 for n <= 32 terms, else a
+// fixed-shape tree (chunks of 256, zero-padded, folded pairwise, then the
+// chunk sums the same way) -- the device's grid CG order.
+double standin_sum(std::vector<double>& q, std::size_t n) {
+    if (n <= 32) {
+        double s = 0.0;
+        for (std::size_t i = 0; i < n; ++i) s += q[i];
+        return s;
+    }
+    while (n > 1) {
+        const std::size_t nc = (n + 255) / 256;
+        for (std::size_t c = 0; c < nc; ++c) {
+            double t[256];
+            for (std::size_t j = 0; j < 256; ++j) t[j] = c * 256 + j < n ? q[c * 256 + j] : 0.0;
+            for (int h = 128; h >= 1; h >>= 1)
+                for (int j = 0; j < h; ++j) t[j] = t[j] + t[j + h];
+            q[c] = t[0];
+        }
+        n = nc;
+    }
+    return q[0];
+}
+
 std::vector<double> coarse_cg(const CsrCopy& A, const std::vector<double>& w, double wtotal,
                               const std::vector<double>& b, bool project) {
     const int n = A.n;
-    std::vector<double> rhs(b);
+    std::vector<double> rhs(b), q(n);
     if (project) {
-        double m = 0.0;
-        for (int i = 0; i < n; ++i) m += w[i] * b[i];
-        m = m / wtotal;
+        for (int i = 0; i < n; ++i) q[i] = w[i] * b[i];
+        const double m = standin_sum(q, n) / wtotal;
         for (int i = 0; i < n; ++i) rhs[i] = b[i] - m;
     }
     std::vector<double> x(n, 0.0), r(rhs), p(rhs), Ap(n);
-    double rr = 0.0;
-    for (int i = 0; i < n; ++i) rr += (w[i] * r[i]) * r[i];
+    for (int i = 0; i < n; ++i) q[i] = (w[i] * r[i]) * r[i];
+    double rr = standin_sum(q, n);
     const double rr0 = rr;
     const int maxit = 4 * n + 20;
     for (int it = 0; it < maxit; ++it) {
@@ -66,22 +88,21 @@ std::vector<double> coarse_cg(const CsrCopy& A, const std::vector<double>& w, do
             for (int k = A.rp[i]; k < A.rp[i + 1]; ++k) s += A.v[k] * p[A.ci[k]];
             Ap[i] = s;
         }
-        double curv = 0.0;
-        for (int i = 0; i < n; ++i) curv += (w[i] * p[i]) * Ap[i];
+        for (int i = 0; i < n; ++i) q[i] = (w[i] * p[i]) * Ap[i];
+        const double curv = standin_sum(q, n);
         if (curv == 0.0) break;
         const double alpha = rr / curv;
         for (int i = 0; i < n; ++i) x[i] = x[i] + alpha * p[i];
         for (int i = 0; i < n; ++i) r[i] = r[i] - alpha * Ap[i];
-        double rn = 0.0;
-        for (int i = 0; i < n; ++i) rn += (w[i] * r[i]) * r[i];
+        for (int i = 0; i < n; ++i) q[i] = (w[i] * r[i]) * r[i];
+        const double rn = standin_sum(q, n);
         const double beta = rn / rr;
         for (int i = 0; i < n; ++i) p[i] = r[i] + beta * p[i];
         rr = rn;
     }
     if (project) {
-        double ym = 0.0;
-        for (int i = 0; i < n; ++i) ym += w[i] * x[i];
-        ym = ym / wtotal;
+        for (int i = 0; i < n; ++i) q[i] = w[i] * x[i];
+        const double ym = standin_sum(q, n) / wtotal;
         for (int i = 0; i < n; ++i) x[i] = x[i] - ym;
     }
     return x;

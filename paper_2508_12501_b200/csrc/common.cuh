@@ -158,6 +158,7 @@ struct decmg_gpu_ctx {
     double* hsmall = nullptr;   // pinned host mirror
     double* hsmall_dev = nullptr;  // its device alias (mapped pinned memory)
     double* coarse_scratch = nullptr;
+    double* cg_grid_buf = nullptr;  // coarse grid CG (n > 32): per-lane scalars + tree partials, on first use
     double* bproj = nullptr;    // projected RHS for solve [n0][max_nrhs]
     double* xsol = nullptr;     // solve snapshot [n0][max_nrhs]
     double* hist_dev = nullptr; // [hist_cap][max_nrhs]

@@ -346,14 +346,40 @@ struct Driver {
         double* x = xcur(L);
         const double* b = bptr(k);
         const int project = c->dirichlet ? 0 : 1;
-        DG_TRY(launch(c, kCoarseSolve, 0.0, [&] {
-            if (L.nv <= 32)  // one warp per right-hand side
+        if (L.nv <= 32) {  // one warp per right-hand side
+            DG_TRY(launch(c, kCoarseSolve, 0.0, [&] {
                 k_coarse_cg_warp<<<(nrhs + 7) / 8, 256, 0, c->stream>>>(L.nv, nrhs, L.L_rp, L.L_ci, L.L_v, L.area,
                                                                          L.wtot, project, b, x);
-            else
-                k_coarse_cg<<<1, 32, 0, c->stream>>>(L.nv, nrhs, L.L_rp, L.L_ci, L.L_v, L.area, L.wtot,
-                                                     project, b, x, c->coarse_scratch);
-        }));
+            }));
+        } else {  // the tree-sum CG over a cooperative grid
+            const int nchunks = (L.nv + kCgChunk - 1) / kCgChunk;
+            if (!c->cg_grid_buf) DG_TRY(dalloc(c, &c->cg_grid_buf, 2 * static_cast<size_t>(nchunks) * 32 + 256));
+            const size_t nv = static_cast<size_t>(L.nv) * nrhs;
+            CoarseGridArgs a{L.nv, nrhs, project, L.L_rp, L.L_ci, L.L_v, L.area, L.wtot, b, x,
+                             c->coarse_scratch, c->coarse_scratch + nv, c->coarse_scratch + 2 * nv,
+                             c->coarse_scratch + 3 * nv, c->cg_grid_buf + 256, c->cg_grid_buf};
+            const size_t smem = static_cast<size_t>(kCgChunk) * nrhs * sizeof(double);
+            const void* fn = reinterpret_cast<const void*>(k_coarse_cg_grid);
+            if (first_on_device(c, fn))
+                DG_CUDA(cudaFuncSetAttribute(k_coarse_cg_grid, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(kCgChunk * 32 * sizeof(double))));
+            const int per_sm = block_occupancy(c, fn, kCgChunk, kCgChunk * 32 * sizeof(double));
+            if (per_sm < 1) return Status::Err(DECMG_CUDA, "coarse CG kernel does not fit on an SM");
+            const int g = std::min(nchunks, per_sm * c->num_sms);
+            DG_TRY(launch(c, kCoarseSolve, 0.0, [&] {
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(g);
+                cfg.blockDim = dim3(kCgChunk);
+                cfg.dynamicSmemBytes = smem;
+                cfg.stream = c->stream;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeCooperative;
+                at[0].val.cooperative = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                cudaLaunchKernelEx(&cfg, k_coarse_cg_grid, a);
+            }));
+        }
         L.x_zero = false;
         return Status::Ok();
     }
@@ -366,6 +392,7 @@ struct Driver {
         const int Lc = static_cast<int>(c->lv.size());
         const int m = Lc - 1 - level;
         if (!c->vtail || level < 1 || m < 1 || m >= kTailMax || tpr > 8 || fuse_hist) return false;
+        if (c->lv.back().nv > 32) return false;  // larger coarse solves run the tree-sum grid CG
         if (plan.smoother != DECMG_SMOOTHER_JACOBI) return false;
         if (static_cast<int64_t>(c->lv[level].nv) * nrhs > c->vtail_items) return false;
         if (w + 2 * m > static_cast<int>(plan.walk.size())) return false;

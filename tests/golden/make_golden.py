@@ -68,6 +68,22 @@ SOLVES = [
     ("solve_ico_cubic_3_ylm", ["solve", "ico+cubic", "3", "neumann", "ylm", "1", "1e-8", "300"]),
     ("solve_square_cubic_4_uniform", ["solve", "square+cubic", "4", "neumann", "uniform", "5", "1e-8", "300"]),
     ("solve_config2_cg", ["solve", "ico", "6", "neumann", "ylm", "1", "1e-8", "200", "cg"]),
+    # build_hierarchy's use_levels (multigrid.cpp:333-337), the paper's "as more levels are used"
+    # experiment (625-vertex equilateral base, W-cycles, Gauss-Seidel), x3 here:
+    # coarse solves of 9,409 / 2,401 / 625 unknowns (the stand-in's tree-sum CG above 32)
+    ("solve_levels_used_2", ["solve", "equi:24:48:1.0", "3", "neumann", "uniform", "7", "1e-8", "60", "gs", "2",
+                             "rediscretize", "W", "2", "2"]),
+    ("solve_levels_used_3", ["solve", "equi:24:48:1.0", "3", "neumann", "uniform", "7", "1e-8", "60", "gs", "3",
+                             "rediscretize", "W", "2", "2"]),
+    ("solve_levels_used_all", ["solve", "equi:24:48:1.0", "3", "neumann", "uniform", "7", "1e-8", "60", "gs", "0",
+                               "rediscretize", "W", "2", "2"]),
+    ("solve_square_dirichlet_levels_used", ["solve", "square", "6", "dirichlet", "sinsin", "0", "1e-8", "60", "jacobi",
+                                            "3"]),
+    # HierarchyOptions (multigrid.hpp:99-104): Galerkin coarse operators, clamped dual areas
+    # (Galerkin diverges on the flat meshes in the reference itself; the icosphere converges)
+    ("solve_ico_4_galerkin", ["solve", "ico", "4", "neumann", "uniform", "5", "1e-8", "100", "gs", "0", "galerkin"]),
+    ("solve_ico_5_clamp", ["solve", "ico", "5", "neumann", "uniform", "5", "1e-8", "200", "jacobi", "0", "clamp"]),
+    ("solve_square_5_gs", ["solve", "square", "5", "neumann", "uniform", "5", "1e-8", "200", "gs"]),
 ]
 PCG = [
     # gmg_preconditioned_cg (solvers.cpp:118-130): <rhs> <seed> <V|W> <pre> <post> <cycles> <tol> <maxit> [smoother]
