@@ -200,6 +200,7 @@ struct decmg_gpu_ctx {
     int64_t vtail_items = 262144;  // ... from the first level with at most this many rows x RHS (env DECMG_VTAIL_ITEMS)
     cudaStream_t cap_stream = nullptr;
     double* gstate_raw = nullptr;  // SolveState (rowkernels.cuh) of the device loop
+    int* hcnt = nullptr;           // history slot counter of run_cycle's replayed bodies (cycle.cu run_graph)
     std::vector<cudaEvent_t> io_events;
     int64_t launch_count = 0;
     int rpt = 4;                // right-hand sides per thread in the vector mapping (env DECMG_RPT)

@@ -69,6 +69,82 @@ Status make_plan(const decmg_gpu_ctx* c, const decmg_gpu_plan* p, Plan* out) {
     return Status::Ok();
 }
 
+namespace {
+
+// hist[(*cnt) * nrhs + l] = res[l]; ++*cnt (the history slot of a replayed body)
+__global__ void k_hist_put(int nrhs, const double* __restrict__ res, double* __restrict__ hist, int* cnt) {
+    const int l = threadIdx.x;
+    const int c = *cnt;
+    if (l < nrhs) hist[static_cast<int64_t>(c) * nrhs + l] = res[l];
+    __syncwarp();
+    if (l == 0) *cnt = c + 1;
+}
+
+// run_cycle's cycles 1 .. ncycles-1 as replays of one captured body: the first
+// level-0 sweep with the fused residual norm of the incoming iterate, its
+// history store (slot from a device counter), the rest of the cycle. Valid
+// when the body keeps level 0's ping-pong parity (checked after the capture,
+// as in solve_graph); hist rows 0 .. ncycles-1 end up in d_hist.
+Status run_graph(decmg_gpu_ctx* c, Driver& dr, const Plan& plan, int nrhs, double* denom, int ncycles,
+                 double* d_hist, bool* graphed) {
+    *graphed = false;
+    if (!c->hcnt) DG_TRY(dalloc(c, &c->hcnt, 1));
+    double* dres = c->dsmall + 256;
+    uint64_t omega_bits = 0;
+    std::memcpy(&omega_bits, &plan.omega, sizeof omega_bits);
+    std::string key = "run|" + plan.walk + "|" + std::to_string(plan.smoother) + "|" + std::to_string(omega_bits) +
+                      "|" + std::to_string(nrhs) + "|" + std::to_string(reinterpret_cast<uintptr_t>(dr.b0)) + "|" +
+                      std::to_string(reinterpret_cast<uintptr_t>(d_hist)) + "|";
+    for (size_t k = 0; k < c->lv.size(); ++k)
+        key += std::to_string(plan.pre[k]) + "," + std::to_string(plan.post[k]) + "," +
+               std::to_string(c->lv[k].cur) + std::to_string(c->lv[k].x_zero ? 1 : 0) + ";";
+    cudaGraphExec_t exec = nullptr;
+    for (auto& e : c->graphs)
+        if (e.key == key) exec = e.exec;
+    if (!exec) {
+        std::vector<std::pair<int, bool>> st0;
+        for (const Level& L : c->lv) st0.emplace_back(L.cur, L.x_zero);
+        DG_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        dr.fuse_hist = dres;
+        dr.fuse_denom = denom;
+        dr.fuse_hook = [&](const double*, bool* stop) -> Status {
+            *stop = false;
+            return launch(c, kNorms, 0.0, [&] { k_hist_put<<<1, 32, 0, c->stream>>>(nrhs, dres, d_hist, c->hcnt); });
+        };
+        Status hs = dr.one_cycle(plan);
+        dr.fuse_hook = nullptr;
+        const bool fused = dr.fuse_hist == nullptr;
+        dr.fuse_hist = nullptr;
+        cudaGraph_t g = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+        if (hs.ok() && e != cudaSuccess) hs = cuda_status(e, "graph capture (run_cycle body)");
+        if (!hs.ok()) {
+            if (g) cudaGraphDestroy(g);
+            return hs;
+        }
+        if (!fused || c->lv[0].cur != st0[0].first) {  // no fused norm, or a parity-flipping walk: eager loop
+            cudaGraphDestroy(g);
+            for (size_t k = 0; k < c->lv.size(); ++k) {
+                c->lv[k].cur = st0[k].first;
+                c->lv[k].x_zero = st0[k].second;
+            }
+            return Status::Ok();
+        }
+        DG_CUDA(cudaGraphInstantiate(&exec, g, 0));
+        c->graphs.push_back({key, g, exec});
+    }
+    DG_CUDA(cudaMemsetAsync(c->hcnt, 0, sizeof(int), c->stream));
+    for (int k = 1; k < ncycles; ++k) {
+        DG_CUDA(cudaGraphLaunch(exec, c->stream));
+        ++c->launch_count;
+    }
+    DG_TRY(dr.resnorm(d_hist + static_cast<int64_t>(ncycles - 1) * nrhs, denom));
+    *graphed = true;
+    return Status::Ok();
+}
+
+}  // namespace
+
 Status run_cycles(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, const double* d_x0,
                   int ncycles, double* d_x, double* d_hist) {
     DG_TRY(check_nrhs(c, nrhs));
@@ -84,7 +160,17 @@ Status run_cycles(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_
     DG_TRY(dr.make_denom(denom));
     // hist[c] = residual of the iterate after cycle c: computed by the first
     // level-0 sweep of cycle c+1 when possible, else by a separate pass.
-    for (int cyc = 0; cyc < ncycles; ++cyc) {
+    int cyc = 0;
+    if (ncycles >= 3 && c->graph && !c->timing.enabled && c->lv.size() > 1) {
+        // cycles 1 .. ncycles-1 as replays of one captured body (run_graph)
+        DG_TRY(dr.one_cycle(plan));
+        cyc = 1;
+        bool graphed = false;
+        if (dr.can_fuse(plan)) DG_TRY(run_graph(c, dr, plan, nrhs, denom, ncycles, d_hist, &graphed));
+        if (graphed) cyc = ncycles;
+        else DG_TRY(dr.resnorm(d_hist, denom));  // hist[0] of the eager loop below
+    }
+    for (; cyc < ncycles; ++cyc) {
         DG_TRY(dr.one_cycle(plan));
         double* hc = d_hist + static_cast<int64_t>(cyc) * nrhs;
         if (cyc + 1 < ncycles && dr.can_fuse(plan)) {
