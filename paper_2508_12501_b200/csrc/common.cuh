@@ -198,6 +198,9 @@ struct decmg_gpu_ctx {
     int carveout = 50;
     int vtail = 1;              // bottom of the V in one cooperative kernel (env DECMG_VTAIL=0: per-pass kernels)
     int64_t vtail_items = 262144;  // ... from the first level with at most this many rows x RHS (env DECMG_VTAIL_ITEMS)
+    int vtail_cta_items = 2048;    // ... levels with at most this many thread items on CTA 0 alone (env DECMG_VTAIL_CTA)
+    int vtail_ctas_per_sm = 1;     // ... resident CTAs per SM, at most (env DECMG_VTAIL_CTAS)
+    unsigned long long* vtail_trace = nullptr;  // per-pass %globaltimer stamps (env DECMG_VTAIL_TRACE=1)
     cudaStream_t cap_stream = nullptr;
     double* gstate_raw = nullptr;  // SolveState (rowkernels.cuh) of the device loop
     int* hcnt = nullptr;           // history slot counter of run_cycle's replayed bodies (cycle.cu run_graph)

@@ -415,14 +415,14 @@ struct Driver {
         a.nrhs = nrhs;
         a.project = c->dirichlet ? 0 : 1;
         a.omega = plan.omega;
-        a.r = c->r;
         const Level& Cst = c->lv[Lc - 1];
         a.crp = Cst.L_rp;
         a.cci = Cst.L_ci;
         a.cv = Cst.L_v;
         a.carea = Cst.area;
         a.cwtot = Cst.wtot;
-        a.cscratch = c->coarse_scratch;
+        a.cta_items = c->vtail_cta_items;
+        a.trace = c->vtail_trace;
         for (int i = 0; i < nl; ++i) {
             const Level& L = c->lv[level + i];
             TailLevel& T = a.lv[i];
@@ -450,7 +450,10 @@ struct Driver {
         Status st;
         DISPATCH_BP(key, {
             auto kern = k_vtail<BP, RPT>;
-            const int blocks = block_occupancy(c, reinterpret_cast<const void*>(kern), kBlock, 0) >= 1 ? c->num_sms : 0;
+            // every resident CTA (the passes of mid-size levels are latency-bound)
+            const int per_sm = std::min(block_occupancy(c, reinterpret_cast<const void*>(kern), kBlock, 0),
+                                        c->vtail_ctas_per_sm);
+            const int blocks = per_sm >= 1 ? per_sm * c->num_sms : 0;
             if (blocks == 0) {
                 st = Status::Err(DECMG_CUDA, "bottom-of-V kernel does not fit on an SM");
             } else {
