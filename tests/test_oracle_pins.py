@@ -81,7 +81,12 @@ def test_cycles_match_reference_bitwise(stem):
     assert str(fnv(x)) == g["fnv_x"]
 
 
-SOLVE = sorted(p.stem for p in GOLDEN.glob("solve_*.json"))
+# The oracle restates the default hierarchy (rediscretised, every level, no
+# clamp) with a V(2,2) walk; goldens that set HierarchyOptions, use_levels or
+# another walk (argv beyond the smoother) are checked against the device path
+# directly (tests/test_gpu_parity.py::test_gmg_solve_vs_reference,
+# tests/test_gpu_shim.py).
+SOLVE = sorted(p.stem for p in GOLDEN.glob("solve_*.json") if len(load(p.stem)["_argv"]) <= 9)
 
 
 @pytest.mark.parametrize("stem", SOLVE)
