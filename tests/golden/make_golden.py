@@ -135,6 +135,32 @@ def make_io():
     (OUT / "io.json").write_text(json.dumps(out, indent=1) + "\n")
 
 
+# The downstream consumer (integrate_convection, physics.cpp:220-272): the
+# reference on the CPU, oracle/_ref/convection_ref (`make -C oracle convection`).
+# argv: nx ny levels t_final samples smoother cycle pre post solver [rtol=atol]
+CONVECTION = [
+    ("convection_32_gs_w33", ["32", "32", "3", "0.002", "3", "gs", "W", "3", "3", "gmg", "1e-7"]),
+    ("convection_32_jacobi_v22", ["32", "32", "3", "0.002", "3", "jacobi", "V", "2", "2", "gmg", "1e-7"]),
+    ("convection_64_sgs_f21", ["64", "32", "4", "0.001", "2", "sgs", "F", "2", "1", "gmg", "1e-6"]),
+    ("convection_32_pcg", ["32", "32", "3", "0.001", "2", "gs", "W", "3", "3", "gmgpcg", "1e-7"]),
+    ("convection_256_gs_w33", ["256", "256", "6", "0.00002", "2", "gs", "W", "3", "3", "gmg", "1e-6"]),
+]
+
+
+def make_convection(only):
+    exe = ROOT / "oracle" / "_ref" / "convection_ref"
+    if not exe.exists():
+        subprocess.run(["make", "-C", str(ROOT / "oracle"), "convection", "-j8"], check=True)
+    for stem, argv in CONVECTION:
+        if only and stem not in only:
+            continue
+        res = subprocess.run([str(exe), *argv], check=True, capture_output=True, text=True)
+        data = json.loads(res.stdout)
+        data["_argv"] = argv
+        (OUT / f"{stem}.json").write_text(json.dumps(data, separators=(",", ":")) + "\n")
+        print(stem, file=sys.stderr)
+
+
 def run(argv):
     res = subprocess.run([str(HARNESS), *argv], check=True, capture_output=True, text=True)
     return json.loads(res.stdout)
@@ -146,6 +172,7 @@ def main() -> int:
     only = set(sys.argv[1:])  # optional: regenerate just these stems
     if not only or "io" in only:
         make_io()
+    make_convection(only)
     for stem, argv in STRUCTURE + CYCLES + SOLVES + PCG:
         if only and stem not in only:
             continue
