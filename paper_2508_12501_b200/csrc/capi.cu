@@ -51,6 +51,11 @@ Status init_ctx(decmg_gpu_ctx* c, const decmg_gpu_config* cfg) {
     if (const char* e = std::getenv("DECMG_VTAIL_TRACE"))
         if (std::atoi(e)) DG_TRY(dalloc(c, &c->vtail_trace, 256));
     if (const char* e = std::getenv("DECMG_PFL")) c->pfl = std::atoi(e);
+    if (const char* e = std::getenv("DECMG_PAIR")) c->pair = std::atoi(e);
+    if (const char* e = std::getenv("DECMG_PAIR_GROUP")) c->pair_group = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("DECMG_PAIR_AHEAD")) c->pair_ahead = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("DECMG_PAIR_MIN_ROUNDS")) c->pair_min_rounds = std::max(2, std::atoi(e));
+    if (const char* e = std::getenv("DECMG_TGROUP")) c->tile_group = std::max(-1, std::atoi(e));
     if (const char* e = std::getenv("DECMG_KERNEL")) {
         const std::string m(e);
         c->kmode = m == "pipe" ? 0 : (m == "ell" ? 1 : 2);
@@ -391,7 +396,7 @@ int64_t decmg_gpu_export(decmg_gpu_ctx* ctx, int level, const char* name, void* 
     else if (s == "boundary") pick(m.bd, m.nv, 4);
     else if (s == "diag") pick(m.diag, m.nv, 8);
     else if (s == "order") pick(m.ord, m.nv, 4);
-    else if (s == "vtail_trace") pick(ctx->vtail_trace, 256, 8);  // diagnostics (DECMG_VTAIL_TRACE=1)
+    else if (s == "vtail_trace") pick(ctx->vtail_trace, 256, 8);
     else if (s == "L_row_ptr") pick(m.L_rp, m.nv + 1, 4);
     else if (s == "L_col_idx") pick(m.L_ci, m.nnzL, 4);
     else if (s == "L_values") pick(m.L_v, m.nnzL, 8);

@@ -119,6 +119,15 @@ struct Level {
     int* gsr_rows = nullptr;
     std::vector<int> gsf_ptr, gsr_ptr;
     int* Re_row = nullptr;   // coarse row q per ELL row of Re (-1 = padding)
+    // Plans of the two-sweep pass k_sweep_pair (driver.cuh prepare_pairs), one per tile shape
+    // (rows per tile, set by the number of right-hand sides); grid == 0: the level keeps separate sweeps
+    struct PairPlan {
+        int rows = 0, grid = 0, group = 0, ahead = 0, rounds = 0, ndefer = 0;
+        int* ord2 = nullptr;      // Le_row with the deferred rows set to -1
+        int* defer = nullptr;     // deferred ELL rows, ascending
+        unsigned* count = nullptr;  // [rounds] round counters
+    };
+    std::vector<PairPlan> pair_plans;
     int zero_diag_row = -1;  // first row with L_ii == 0 (-1: none)
     double wtot = 0.0;       // sum of dual areas, sequential (coarse solve)
     // work vectors [nv][max_nrhs]
@@ -210,6 +219,12 @@ struct decmg_gpu_ctx {
     double wtot0 = 0.0;         // sum of level-0 dual areas in the reference order
     int num_sms = 148;
     int pf = 56;                // row-kernel prefetch distance in rows, 0 = off (env DECMG_PF)
+    int tile_group = -1;        // row-kernel tiles per round-robin group (-1: auto, 0: contiguous range per CTA; env DECMG_TGROUP)
+    int pair = 1;               // two Jacobi sweeps per pass where a level has enough rounds (env DECMG_PAIR=0: one sweep per launch)
+    int pair_group = 0;         // tiles per group of the two-sweep pass (0: auto, a ~45 MB round; env DECMG_PAIR_GROUP)
+    int pair_ahead = 0;         // rounds ahead sweep 2 may gather from (env DECMG_PAIR_AHEAD)
+    bool batch_overlap = false; // inside solve_batches with concurrent staging: no cooperative two-sweep passes
+    int pair_min_rounds = 8;    // levels with fewer rounds keep separate sweeps (env DECMG_PAIR_MIN_ROUNDS)
     int pfl = 2;                // prefetch into L1 (1) or L2 (2) (env DECMG_PFL)
     int kmode = 2;              // row kernels: 2 auto (default), 0 pipelined, 1 high-occupancy (env DECMG_KERNEL)
     decmg_gpu::Timing timing;

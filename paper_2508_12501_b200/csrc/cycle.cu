@@ -94,7 +94,7 @@ Status run_graph(decmg_gpu_ctx* c, Driver& dr, const Plan& plan, int nrhs, doubl
     std::memcpy(&omega_bits, &plan.omega, sizeof omega_bits);
     std::string key = "run|" + plan.walk + "|" + std::to_string(plan.smoother) + "|" + std::to_string(omega_bits) +
                       "|" + std::to_string(nrhs) + "|" + std::to_string(reinterpret_cast<uintptr_t>(dr.b0)) + "|" +
-                      std::to_string(reinterpret_cast<uintptr_t>(d_hist)) + "|";
+                      std::to_string(reinterpret_cast<uintptr_t>(d_hist)) + "|" + (dr.use_pairs ? "p|" : "s|");
     for (size_t k = 0; k < c->lv.size(); ++k)
         key += std::to_string(plan.pre[k]) + "," + std::to_string(plan.post[k]) + "," +
                std::to_string(c->lv[k].cur) + std::to_string(c->lv[k].x_zero ? 1 : 0) + ";";
@@ -153,7 +153,7 @@ Status run_cycles(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_
     const double* b_in = d_b;
     if (L.ord || (reinterpret_cast<uintptr_t>(d_b) & 31) != 0) b_in = L.b;  // internal copy (32-byte aligned)
     Driver dr{c, nrhs, bp_of(nrhs), b_in};
-    dr.init();
+    DG_TRY(dr.init());
     if (b_in != d_b) DG_TRY(dr.to_internal(d_b, L.b));
     double* denom = c->dsmall;
     DG_TRY(dr.load_x0(d_x0));
@@ -355,7 +355,7 @@ Status solve_graph(decmg_gpu_ctx* c, Driver& dr, const Plan& plan, int nrhs, uns
                       std::to_string(nrhs) + "|" + std::to_string(reinterpret_cast<uintptr_t>(dr.b0)) + "|" +
                       std::to_string(reinterpret_cast<uintptr_t>(c->hist_dev)) + "|" +
                       std::to_string(reinterpret_cast<uintptr_t>(c->tstamp_dev)) + "|" +
-                      std::to_string(reinterpret_cast<uintptr_t>(c->red)) + "|";
+                      std::to_string(reinterpret_cast<uintptr_t>(c->red)) + "|" + (dr.use_pairs ? "p|" : "s|");
     for (size_t k = 0; k < c->lv.size(); ++k)
         key += std::to_string(plan.pre[k]) + "," + std::to_string(plan.post[k]) + "," +
                std::to_string(c->lv[k].cur) + std::to_string(c->lv[k].x_zero ? 1 : 0) + ";";
@@ -504,7 +504,10 @@ Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, co
         bsrc = c->bproj;
     }
     Driver dr{c, nrhs, bp_of(nrhs), L0.ord ? L0.b : bsrc};
-    dr.init();
+    // a batch stream stages the next batch on other streams while this one cycles: the two-sweep
+    // pass is a cooperative launch (every CTA resident), which would wait for those kernels to drain
+    dr.use_pairs = !c->batch_overlap;
+    DG_TRY(dr.init());
     if (L0.ord) DG_TRY(dr.to_internal(bsrc, L0.b));
     double* denom = c->dsmall;
     double* dres = c->dsmall + 256;
@@ -671,6 +674,11 @@ Status solve_batches(decmg_gpu_ctx* c, const Plan& plan, int nrhs, int nbatch, c
         c->stream = keep;
         return s;
     };
+    struct Overlap {  // the solves of this call run beside the staging of the next batch
+        decmg_gpu_ctx* c;
+        explicit Overlap(decmg_gpu_ctx* cc, bool on) : c(cc) { c->batch_overlap = on; }
+        ~Overlap() { c->batch_overlap = false; }
+    } overlap(c, nbatch > 1 && !c->proj_seq);
     DG_CUDA(cudaEventRecord(c->ev_start, c->stream));  // after everything already queued on the context
     DG_CUDA(cudaStreamWaitEvent(c->aux_stream, c->ev_start, 0));
     DG_CUDA(cudaStreamWaitEvent(c->d2h_stream, c->ev_start, 0));
@@ -711,7 +719,7 @@ Status smooth_level(decmg_gpu_ctx* c, int k, const Plan& plan, int iters, int nr
     if ((plan.smoother == DECMG_SMOOTHER_GS || plan.smoother == DECMG_SMOOTHER_SGS) && !m.gsf_rows)
         DG_TRY(build_gs_schedule(c, m));  // the coarsest level has none until asked
     Driver dr{c, nrhs, bp_of(nrhs), c->lv[0].b};
-    dr.init();
+    DG_TRY(dr.init());
     const int64_t t = static_cast<int64_t>(m.nv) * nrhs;
     auto perm = [&](const double* src, double* dst, bool scatter) -> Status {
         if (!m.ord) {

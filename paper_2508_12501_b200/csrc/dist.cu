@@ -1126,6 +1126,7 @@ Status dist_run(decmg_gpu_dist* D, const Plan& plan, int nrhs, const double* h_b
     DistDriver dd{D, nrhs, {}};
     for (size_t i = 0; i < D->ranks.size(); ++i) {
         Driver dr{g, nrhs, bp_of(nrhs), g->lv[0].b};
+        dr.use_pairs = false;
         dr.init();
         dd.drv.push_back(dr);
     }
@@ -1135,6 +1136,7 @@ Status dist_run(decmg_gpu_dist* D, const Plan& plan, int nrhs, const double* h_b
     if (solve && !g->dirichlet) DG_TRY(project_compatible(g, nrhs, g->io_b));
     {  // ||b|| over the internal numbering, exactly as the single-GPU run
         Driver d0{g, nrhs, bp_of(nrhs), g->lv[0].b};
+        d0.use_pairs = false;
         d0.init();
         DG_TRY(d0.to_internal(g->io_b, g->lv[0].b));
         DG_TRY(d0.make_denom(g->dsmall));

@@ -5,6 +5,12 @@
 
 #include "rowkernels.cuh"
 
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
 #include <functional>
 #include <string>
 #include <type_traits>
@@ -30,12 +36,166 @@ struct Driver {
     std::function<Status(const double*, bool*)> fuse_hook;
     bool stopped = false;
     const double* cg_weights = nullptr;  // CG smoother inner-product weights (nullptr: the level's dual areas)
+    bool use_pairs = true;  // two Jacobi sweeps per pass where planned (the partitioned path exchanges halos between sweeps)
 
-    void init() {
+    Status init() {
         const bool vec = nrhs == bp && bp >= 2;
         int rpt = vec ? (bp < c->rpt ? bp : c->rpt) : 1;
         key = 10 * bp + rpt;
         tpr = bp / rpt;
+        return prepare_pairs();
+    }
+
+    // ---- two Jacobi sweeps per pass (rowkernels.cuh k_sweep_pair) ----------
+    // Grid and plan of the pass for level k at this driver's tile shape, built on
+    // first use and cached in the level: called from the API entry points before
+    // any capture (it allocates and synchronises). pair_rows stays 0 where the
+    // level has too few rounds or no ELL operator.
+    template <int BP, int RPT, int W>
+    Status prepare_pair_level(Level& L) {
+        using G = PipeGeom<BP, RPT, W>;
+        Level::PairPlan P;
+        P.rows = G::ROWS;
+        auto kern = k_sweep_pair<BP, RPT, W, false>;
+        auto kern_n = k_sweep_pair<BP, RPT, W, true>;
+        for (const void* fn : {reinterpret_cast<const void*>(kern), reinterpret_cast<const void*>(kern_n)})
+            if (first_on_device(c, fn)) {
+                DG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(G::PSMEM)));
+                if (c->carveout >= 0 && kPipeCtasPerSm * (G::PSMEM + 1024.0) <= c->carveout / 100.0 * kSmemPerSm)
+                    DG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, c->carveout));
+            }
+        const int occ = std::min(block_occupancy(c, reinterpret_cast<const void*>(kern_n), kPipeThreads, G::PSMEM),
+                                 block_occupancy(c, reinterpret_cast<const void*>(kern), kPipeThreads, G::PSMEM));
+        const int grid = std::min(occ, kPipeCtasPerSm) * c->num_sms;
+        // a round (grid * group tiles, both sweeps' traffic) of about 45 MB: sweep 2 finds b, the
+        // operator tiles and sweep 1's output of its round still in L2 (measured: 112 rows per
+        // group with 16 right-hand sides, 448 with one)
+        const double round_bytes = 2.0 * (24.0 * nrhs + 12.0 * W + 4.0) * G::ROWS * std::max(grid, 1);
+        const int group = c->pair_group > 0 ? c->pair_group : std::max(1, static_cast<int>(45.0e6 / round_bytes + 0.5));
+        const int ntiles = (L.nv + G::ROWS - 1) / G::ROWS;
+        const int per_round = std::max(grid, 1) * group;
+        const int rounds = (ntiles + per_round - 1) / per_round;
+        if (grid < 1 || rounds < c->pair_min_rounds) {
+            L.pair_plans.push_back(P);  // grid == 0: separate sweeps
+            return Status::Ok();
+        }
+        const int npad = (L.nv + 223) / 224 * 224;
+        DG_TRY(dalloc(c, &P.ord2, npad));
+        DG_TRY(dalloc(c, &P.count, rounds));
+        unsigned char* flag = nullptr;
+        int *nsel = nullptr, *sel = nullptr;
+        void* tmp = nullptr;
+        DG_CUDA(cudaMalloc(&flag, npad));
+        DG_CUDA(cudaMalloc(&nsel, sizeof(int)));
+        DG_CUDA(cudaMalloc(&sel, sizeof(int) * npad));
+        k_pair_plan<<<grid_for(npad, kBlock), kBlock, 0, c->stream>>>(npad, W, per_round * G::ROWS, c->pair_ahead, L.Le_ci,
+                                                                     L.Le_row, P.ord2, flag);
+        size_t bytes = 0;
+        cub::CountingInputIterator<int> ids(0);
+        DG_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, ids, flag, sel, nsel, npad, c->stream));
+        DG_CUDA(cudaMalloc(&tmp, bytes ? bytes : 1));
+        DG_CUDA(cub::DeviceSelect::Flagged(tmp, bytes, ids, flag, sel, nsel, npad, c->stream));
+        int nd = 0;
+        DG_CUDA(cudaMemcpyAsync(&nd, nsel, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        DG_CUDA(cudaStreamSynchronize(c->stream));
+        DG_TRY(dalloc(c, &P.defer, std::max(nd, 1)));
+        DG_CUDA(cudaMemcpyAsync(P.defer, sel, sizeof(int) * nd, cudaMemcpyDeviceToDevice, c->stream));
+        DG_CUDA(cudaStreamSynchronize(c->stream));
+        cudaFree(tmp);
+        cudaFree(sel);
+        cudaFree(nsel);
+        cudaFree(flag);
+        P.ndefer = nd;
+        P.grid = grid;
+        P.group = group;
+        P.ahead = c->pair_ahead;
+        P.rounds = rounds;
+        L.pair_plans.push_back(P);
+        if (std::getenv("DECMG_DEBUG"))
+            std::fprintf(stderr, "[decmg] pair plan: %d rows, %d rows/tile, grid %d, group %d, %d rounds, %d deferred rows\n",
+                         L.nv, G::ROWS, grid, group, rounds, nd);
+        return Status::Ok();
+    }
+    int pair_tile_rows() const {
+        int rows = 0;
+        DISPATCH_BP(key, { rows = PipeGeom<BP, RPT, 7>::ROWS; })
+        return rows;
+    }
+    const Level::PairPlan* pair_plan(const Level& L) const {
+        if (!use_pairs || !c->pair || tpr > 8) return nullptr;
+        const int rows = pair_tile_rows();
+        for (const Level::PairPlan& P : L.pair_plans)
+            if (P.rows == rows) return P.grid > 0 ? &P : nullptr;
+        return nullptr;
+    }
+    Status prepare_pairs() {
+        if (!use_pairs || !c->pair || tpr > 8) return Status::Ok();
+        const int rows = pair_tile_rows();
+        for (size_t k = 0; k + 1 < c->lv.size(); ++k) {
+            Level& L = c->lv[k];
+            if (!L.Le_ci || !L.Le_row || L.zero_diag_row >= 0) continue;
+            bool have = false;
+            for (const Level::PairPlan& P : L.pair_plans) have = have || P.rows == rows;
+            if (have) continue;
+            Status st;
+            DISPATCH_BP(key, { st = L.Le_w == 7 ? prepare_pair_level<BP, RPT, 7>(L) : prepare_pair_level<BP, RPT, 8>(L); })
+            DG_TRY(st);
+        }
+        return Status::Ok();
+    }
+    // x[cur] -> (c->r) -> x[cur ^ 1]: two sweeps, one flip. norm: OP_SWEEP_NORM's partials of the incoming x.
+    Status sweep_pair(int k, const Level::PairPlan& P, const Plan& plan, bool norm) {
+        Level& L = c->lv[k];
+        const double R = nrhs;
+        const double bytes = 2.0 * (12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R);
+        DG_CUDA(cudaMemsetAsync(P.count, 0, sizeof(unsigned) * P.rounds, c->stream));
+        Status st;
+        DISPATCH_BP(key, {
+            PairArgs a{};
+            a.ntiles = (L.nv + P.rows - 1) / P.rows;
+            a.nrhs = nrhs;
+            a.eci = L.Le_ci;
+            a.ev = L.Le_v;
+            a.ord = L.Le_row;
+            a.ord2 = P.ord2;
+            a.x = xcur(L);
+            a.b = bptr(k);
+            a.mid = c->r;
+            a.out = L.x[L.cur ^ 1];
+            a.partial = c->red;
+            a.defer = P.defer;
+            a.ndefer = P.ndefer;
+            a.count = P.count;
+            a.omega = plan.omega;
+            a.n = L.nv;
+            a.pf = c->pf;
+            a.group = P.group;
+            a.ahead = P.ahead;
+            st = launch(c, k == 0 ? kFineSweep : kCoarseLevels, bytes, [&] {
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(P.grid);
+                cfg.blockDim = dim3(kPipeThreads);
+                cfg.stream = c->stream;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeCooperative;
+                at[0].val.cooperative = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                if (L.Le_w == 7) {
+                    cfg.dynamicSmemBytes = PipeGeom<BP, RPT, 7>::PSMEM;
+                    if (norm) cudaLaunchKernelEx(&cfg, k_sweep_pair<BP, RPT, 7, true>, a);
+                    else cudaLaunchKernelEx(&cfg, k_sweep_pair<BP, RPT, 7, false>, a);
+                } else {
+                    cfg.dynamicSmemBytes = PipeGeom<BP, RPT, 8>::PSMEM;
+                    if (norm) cudaLaunchKernelEx(&cfg, k_sweep_pair<BP, RPT, 8, true>, a);
+                    else cudaLaunchKernelEx(&cfg, k_sweep_pair<BP, RPT, 8, false>, a);
+                }
+            });
+        })
+        DG_TRY(st);
+        L.cur ^= 1;
+        L.x_zero = false;
+        return Status::Ok();
     }
 
     const double* bptr(int k) const { return k == 0 ? b0 : c->lv[k].b; }
@@ -51,7 +211,9 @@ struct Driver {
                 int* grid = nullptr) {
         Status st;
         DISPATCH_BP(key, {
-            PipeArgs a{0, nrhs, eci, ev, erow, x, b, out, partial, zr, omega, nrows, c->pf, c->pfl};
+            PipeArgs a{0, nrhs, eci, ev, erow, x, b, out, partial, zr, omega, nrows, c->pf, c->pfl, c->tile_group};
+            // default: groups of ~224 rows (16 right-hand sides) / ~448 rows (a single one)
+            if (a.group < 0) a.group = std::max(1, (nrhs >= 8 ? 224 : 448) / PipeGeom<BP, RPT, W>::ROWS);
             // pipelined kernel for the 7/8-wide operators (L, R), the
             // high-occupancy kernel for P (2-wide rows); env DECMG_KERNEL forces one
             const bool ell = c->kmode == 1 || (c->kmode == 2 && W == 2);
@@ -79,6 +241,9 @@ struct Driver {
                                              cudaFuncAttributePreferredSharedMemoryCarveout, c->carveout);
                 }
                 a.ntiles = ntiles;
+                // round-robin tile groups only where every CTA gets many of them (small
+                // levels keep one contiguous range per CTA: a short last round would unbalance them)
+                if (a.group > 0 && static_cast<int64_t>(ntiles) < 16ll * a.group * g) a.group = 0;
                 st = launch(c, cls, bytes, [&] {
                     k_rowop_pipe<BP, RPT, W, OP><<<g, kPipeThreads, G::PSMEM, c->stream>>>(a);
                 });
@@ -248,6 +413,25 @@ struct Driver {
                     DISPATCH_BP(key, k_sweep_zero<BP, RPT><<<rows_grid(L.nv), kBlock, 0, c->stream>>>(
                                         L.nv, nrhs, L.diag_i, b, xo, plan.omega));
                 }));
+            } else if (const Level::PairPlan* P = it + 2 <= iters ? pair_plan(L) : nullptr) {
+                // two sweeps in one pass; the fused norm is of the x that enters the pair
+                const double* xprev = xcur(L);
+                DG_TRY(sweep_pair(k, *P, plan, fuse_norm));
+                it += 2;
+                if (fuse_norm) {
+                    DG_TRY(reduce_partials(P->grid, fuse_hist, 2, fuse_denom));
+                    fuse_hist = nullptr;
+                    if (fuse_hook) {
+                        bool stop = false;
+                        DG_TRY(fuse_hook(xprev, &stop));
+                        if (stop) {
+                            L.cur ^= 1;  // x_prev stays the current iterate
+                            stopped = true;
+                            return Status::Ok();
+                        }
+                    }
+                }
+                continue;
             } else {
                 const double bytes = 12.0 * L.nnzL + 4.0 * (L.nv + 1) + 24.0 * L.nv * R;
                 const double* x = xcur(L);

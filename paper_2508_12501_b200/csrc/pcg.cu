@@ -62,7 +62,7 @@ Status pcg(decmg_gpu_ctx* c, const Plan& inner, int inner_cycles, int nrhs, cons
         DG_TRY(project_compatible(c, nrhs, c->bproj));
     }
     Driver dr{c, nrhs, bp_of(nrhs), r};
-    dr.init();
+    DG_TRY(dr.init());
     DG_TRY(dr.to_internal(c->bproj, bc));
     // x = 0, r = bc - A 0 = bc exactly
     DG_CUDA(cudaMemsetAsync(x, 0, vb, st));

@@ -36,7 +36,6 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
         : "memory");
 }
 
-
 // Ampere-style async copy of 16 bytes global -> shared (SASS LDGSTS), and an
 // mbarrier arrive that fires when all of this thread's prior cp.async copies
 // have landed (the arrival is pre-counted in the barrier's expected count).
