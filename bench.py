@@ -289,7 +289,10 @@ def run_ours(args, world, rank, local):
     cycle_roofline = {"b_alg_bytes": b_alg, "achieved": cyc_gbs, "unit": "GB/s",
                       "frac_measured_peak": cyc_gbs / measured_peak()[0], "frac_8TBs_spec": cyc_gbs / 8000.0,
                       "note": "compulsory HBM bytes of one batched V(2,2) cycle (fused model) / ms_per_step"}
-    roofline = {"bound": "hbm", "kernel": "k_rowop_pipe<16,4,7,OP_SWEEP> (level-0 weighted-Jacobi sweep)",
+    roofline = {"bound": "hbm", "kernel": "k_sweep_pair<16,4,7> (two level-0 weighted-Jacobi sweeps per launch; the "
+                                          "first sweep of a run from x = 0 is a single k_rowop_pipe launch)",
+                "algorithmic_bytes_note": "SURVEY 8(d) single-sweep bytes x the sweeps of the launch (two); ncu `traffic` is "
+                                          "lower because sweep 2 re-reads b, the operator tiles and sweep 1's output from L2",
                 "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None, "traffic": ncu_traffic(),
                 "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,

@@ -53,6 +53,8 @@ Status init_ctx(decmg_gpu_ctx* c, const decmg_gpu_config* cfg) {
     if (const char* e = std::getenv("DECMG_PFL")) c->pfl = std::atoi(e);
     if (const char* e = std::getenv("DECMG_PAIR")) c->pair = std::atoi(e);
     if (const char* e = std::getenv("DECMG_PAIR_GROUP")) c->pair_group = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("DECMG_PAIR_CTAS")) c->pair_ctas = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("DECMG_PAIR_CTAS_OVERLAP")) c->pair_ctas_overlap = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("DECMG_PAIR_AHEAD")) c->pair_ahead = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("DECMG_PAIR_MIN_ROUNDS")) c->pair_min_rounds = std::max(2, std::atoi(e));
     if (const char* e = std::getenv("DECMG_TGROUP")) c->tile_group = std::max(-1, std::atoi(e));

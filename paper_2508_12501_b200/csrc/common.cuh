@@ -122,7 +122,7 @@ struct Level {
     // Plans of the two-sweep pass k_sweep_pair (driver.cuh prepare_pairs), one per tile shape
     // (rows per tile, set by the number of right-hand sides); grid == 0: the level keeps separate sweeps
     struct PairPlan {
-        int rows = 0, grid = 0, group = 0, ahead = 0, rounds = 0, ndefer = 0;
+        int rows = 0, ctas = 0, grid = 0, group = 0, ahead = 0, rounds = 0, ndefer = 0;  // ctas: CTAs per SM asked for
         int* ord2 = nullptr;      // Le_row with the deferred rows set to -1
         int* defer = nullptr;     // deferred ELL rows, ascending
         unsigned* count = nullptr;  // [rounds] round counters
@@ -223,6 +223,8 @@ struct decmg_gpu_ctx {
     int pair = 1;               // two Jacobi sweeps per pass where a level has enough rounds (env DECMG_PAIR=0: one sweep per launch)
     int pair_group = 0;         // tiles per group of the two-sweep pass (0: auto, a ~45 MB round; env DECMG_PAIR_GROUP)
     int pair_ahead = 0;         // rounds ahead sweep 2 may gather from (env DECMG_PAIR_AHEAD)
+    int pair_ctas = 3;          // resident CTAs per SM of the two-sweep pass (env DECMG_PAIR_CTAS)
+    int pair_ctas_overlap = 0;  // ... inside a batch stream (0: separate sweeps there; env DECMG_PAIR_CTAS_OVERLAP)
     bool batch_overlap = false; // inside solve_batches with concurrent staging: no cooperative two-sweep passes
     int pair_min_rounds = 8;    // levels with fewer rounds keep separate sweeps (env DECMG_PAIR_MIN_ROUNDS)
     int pfl = 2;                // prefetch into L1 (1) or L2 (2) (env DECMG_PFL)

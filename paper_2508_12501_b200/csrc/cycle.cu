@@ -506,7 +506,7 @@ Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, co
     Driver dr{c, nrhs, bp_of(nrhs), L0.ord ? L0.b : bsrc};
     // a batch stream stages the next batch on other streams while this one cycles: the two-sweep
     // pass is a cooperative launch (every CTA resident), which would wait for those kernels to drain
-    dr.use_pairs = !c->batch_overlap;
+    dr.use_pairs = !c->batch_overlap || c->pair_ctas_overlap > 0;
     DG_TRY(dr.init());
     if (L0.ord) DG_TRY(dr.to_internal(bsrc, L0.b));
     double* denom = c->dsmall;

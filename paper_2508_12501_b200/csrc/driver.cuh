@@ -56,6 +56,7 @@ struct Driver {
         using G = PipeGeom<BP, RPT, W>;
         Level::PairPlan P;
         P.rows = G::ROWS;
+        P.ctas = pair_ctas();
         auto kern = k_sweep_pair<BP, RPT, W, false>;
         auto kern_n = k_sweep_pair<BP, RPT, W, true>;
         for (const void* fn : {reinterpret_cast<const void*>(kern), reinterpret_cast<const void*>(kern_n)})
@@ -66,7 +67,7 @@ struct Driver {
             }
         const int occ = std::min(block_occupancy(c, reinterpret_cast<const void*>(kern_n), kPipeThreads, G::PSMEM),
                                  block_occupancy(c, reinterpret_cast<const void*>(kern), kPipeThreads, G::PSMEM));
-        const int grid = std::min(occ, kPipeCtasPerSm) * c->num_sms;
+        const int grid = std::min(occ, pair_ctas()) * c->num_sms;
         // a round (grid * group tiles, both sweeps' traffic) of about 45 MB: sweep 2 finds b, the
         // operator tiles and sweep 1's output of its round still in L2 (measured: 112 rows per
         // group with 16 right-hand sides, 448 with one)
@@ -116,6 +117,9 @@ struct Driver {
                          L.nv, G::ROWS, grid, group, rounds, nd);
         return Status::Ok();
     }
+    // resident CTAs per SM of the two-sweep pass: one fewer beside a batch stream's staging kernels, so
+    // that the cooperative launch finds room without waiting for them to drain
+    int pair_ctas() const { return std::max(1, std::min(kPipeCtasPerSm, c->batch_overlap ? c->pair_ctas_overlap : c->pair_ctas)); }
     int pair_tile_rows() const {
         int rows = 0;
         DISPATCH_BP(key, { rows = PipeGeom<BP, RPT, 7>::ROWS; })
@@ -125,7 +129,7 @@ struct Driver {
         if (!use_pairs || !c->pair || tpr > 8) return nullptr;
         const int rows = pair_tile_rows();
         for (const Level::PairPlan& P : L.pair_plans)
-            if (P.rows == rows) return P.grid > 0 ? &P : nullptr;
+            if (P.rows == rows && P.ctas == pair_ctas()) return P.grid > 0 ? &P : nullptr;
         return nullptr;
     }
     Status prepare_pairs() {
@@ -135,7 +139,7 @@ struct Driver {
             Level& L = c->lv[k];
             if (!L.Le_ci || !L.Le_row || L.zero_diag_row >= 0) continue;
             bool have = false;
-            for (const Level::PairPlan& P : L.pair_plans) have = have || P.rows == rows;
+            for (const Level::PairPlan& P : L.pair_plans) have = have || (P.rows == rows && P.ctas == pair_ctas());
             if (have) continue;
             Status st;
             DISPATCH_BP(key, { st = L.Le_w == 7 ? prepare_pair_level<BP, RPT, 7>(L) : prepare_pair_level<BP, RPT, 8>(L); })
