@@ -204,7 +204,7 @@ struct decmg_gpu_ctx {
     // preferred shared-memory carve-out (%) of the row kernels and the projection kernels (env
     // DECMG_CARVEOUT, -1 = driver default): one common split lets a batch stream's projection blocks share
     // SMs with the persistent V-cycle kernels instead of holding them until they drain (DESIGN.md §5 x6)
-    int carveout = 50;
+    int carveout = 30;
     int vtail = 1;              // bottom of the V in one cooperative kernel (env DECMG_VTAIL=0: per-pass kernels)
     int64_t vtail_items = 262144;  // ... from the first level with at most this many rows x RHS (env DECMG_VTAIL_ITEMS)
     int vtail_cta_items = 2048;    // ... levels with at most this many thread items on CTA 0 alone (env DECMG_VTAIL_CTA)
