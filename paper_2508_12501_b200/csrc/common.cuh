@@ -198,8 +198,10 @@ struct decmg_gpu_ctx {
         std::string key;
         cudaGraph_t graph;
         cudaGraphExec_t exec;
+        int64_t kernels = 0;  // launches recorded into one replay (launch_count advances by this per replay)
     };
     std::vector<GraphEntry> graphs;
+    int64_t last_graph_kernels = 0;  // kernels per iteration of the solve graph launched last
     int graph = 1;              // env DECMG_GRAPH=0: host-driven cycle loop
     // preferred shared-memory carve-out (%) of the row kernels and the projection kernels (env
     // DECMG_CARVEOUT, -1 = driver default): one common split lets a batch stream's projection blocks share

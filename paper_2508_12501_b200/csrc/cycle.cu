@@ -99,11 +99,16 @@ Status run_graph(decmg_gpu_ctx* c, Driver& dr, const Plan& plan, int nrhs, doubl
         key += std::to_string(plan.pre[k]) + "," + std::to_string(plan.post[k]) + "," +
                std::to_string(c->lv[k].cur) + std::to_string(c->lv[k].x_zero ? 1 : 0) + ";";
     cudaGraphExec_t exec = nullptr;
+    int64_t kernels = 0;
     for (auto& e : c->graphs)
-        if (e.key == key) exec = e.exec;
+        if (e.key == key) {
+            exec = e.exec;
+            kernels = e.kernels;
+        }
     if (!exec) {
         std::vector<std::pair<int, bool>> st0;
         for (const Level& L : c->lv) st0.emplace_back(L.cur, L.x_zero);
+        const int64_t lc0 = c->launch_count;
         DG_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         dr.fuse_hist = dres;
         dr.fuse_denom = denom;
@@ -117,6 +122,8 @@ Status run_graph(decmg_gpu_ctx* c, Driver& dr, const Plan& plan, int nrhs, doubl
         dr.fuse_hist = nullptr;
         cudaGraph_t g = nullptr;
         const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+        kernels = c->launch_count - lc0;  // recorded, not run: counted per replay instead
+        c->launch_count = lc0;
         if (hs.ok() && e != cudaSuccess) hs = cuda_status(e, "graph capture (run_cycle body)");
         if (!hs.ok()) {
             if (g) cudaGraphDestroy(g);
@@ -131,12 +138,12 @@ Status run_graph(decmg_gpu_ctx* c, Driver& dr, const Plan& plan, int nrhs, doubl
             return Status::Ok();
         }
         DG_CUDA(cudaGraphInstantiate(&exec, g, 0));
-        c->graphs.push_back({key, g, exec});
+        c->graphs.push_back({key, g, exec, kernels});
     }
     DG_CUDA(cudaMemsetAsync(c->hcnt, 0, sizeof(int), c->stream));
     for (int k = 1; k < ncycles; ++k) {
         DG_CUDA(cudaGraphLaunch(exec, c->stream));
-        ++c->launch_count;
+        c->launch_count += kernels;
     }
     DG_TRY(dr.resnorm(d_hist + static_cast<int64_t>(ncycles - 1) * nrhs, denom));
     *graphed = true;
@@ -360,9 +367,14 @@ Status solve_graph(decmg_gpu_ctx* c, Driver& dr, const Plan& plan, int nrhs, uns
         key += std::to_string(plan.pre[k]) + "," + std::to_string(plan.post[k]) + "," +
                std::to_string(c->lv[k].cur) + std::to_string(c->lv[k].x_zero ? 1 : 0) + ";";
     cudaGraphExec_t exec = nullptr;
+    int64_t kernels = 0;
     for (auto& e : c->graphs)
-        if (e.key == key) exec = e.exec;
+        if (e.key == key) {
+            exec = e.exec;
+            kernels = e.kernels;
+        }
     if (!exec) {
+        const int64_t lc0 = c->launch_count;
         cudaGraph_t g = nullptr;
         DG_CUDA(cudaGraphCreate(&g, 0));
         cudaGraphConditionalHandle hw;
@@ -422,6 +434,8 @@ Status solve_graph(decmg_gpu_ctx* c, Driver& dr, const Plan& plan, int nrhs, uns
         hs = dr.one_cycle(plan);
         dr.fuse_hook = nullptr;
         dr.fuse_hist = nullptr;
+        kernels = c->launch_count - lc0;  // one loop iteration's kernels, recorded not run
+        c->launch_count = lc0;
         cudaGraph_t tmp = nullptr;
         if (split) {
             const cudaError_t e1 = cudaStreamEndCapture(c->cap_stream, &tmp);
@@ -446,11 +460,11 @@ Status solve_graph(decmg_gpu_ctx* c, Driver& dr, const Plan& plan, int nrhs, uns
             return Status::Ok();
         }
         DG_CUDA(cudaGraphInstantiate(&exec, g, 0));
-        c->graphs.push_back({key, g, exec});
+        c->graphs.push_back({key, g, exec, kernels});
     }
     DG_TRY(launch(c, kNorms, 0.0, [&] { k_solve_init<<<1, 1, 0, c->stream>>>(gst, 1, all, max_cycles, tol); }));
     DG_CUDA(cudaGraphLaunch(exec, c->stream));
-    ++c->launch_count;
+    c->last_graph_kernels = kernels;  // solve() multiplies by the iterations the device loop ran
     *graphed = true;
     return Status::Ok();
 }
@@ -565,6 +579,7 @@ Status solve(decmg_gpu_ctx* c, const Plan& plan, int nrhs, const double* d_b, co
             DG_CUDA(cudaStreamSynchronize(c->stream));
             int maxdone = 0;
             for (int l = 0; l < nrhs; ++l) maxdone = std::max(maxdone, st.done[l]);
+            c->launch_count += c->last_graph_kernels * std::max(maxdone - 1, 1);  // the loop's iterations
             for (int k = 1; k <= maxdone; ++k)  // device clock of each check, offset by the host's launch delay
                 c->last_times.push_back(t_launch0 + 1e-9 * static_cast<double>(ts[k] - ts[0]));
             for (int l = 0; l < nrhs; ++l) {

@@ -248,6 +248,7 @@ struct decmg_gpu_dist {
         cudaGraph_t graph;
         cudaGraphExec_t exec;
         std::vector<std::pair<int, bool>> post;  // host ping-pong state after one body
+        int64_t kernels = 0;                     // launches recorded into one replay
     };
     std::vector<GraphEntry> graphs;
     // host staging
@@ -1230,10 +1231,13 @@ Status dist_run(decmg_gpu_dist* D, const Plan& plan, int nrhs, const double* h_b
                 ge = &e;
                 return Status::Ok();
             }
+        const int64_t lc0 = g->launch_count;
         DG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         Status s = body();
         cudaGraph_t gr = nullptr;
         const cudaError_t e = cudaStreamEndCapture(st, &gr);
+        const int64_t kernels = g->launch_count - lc0;  // recorded, not run: counted per replay
+        g->launch_count = lc0;
         const auto s1 = host_state(D);
         set_host_state(D, s0);  // nothing ran yet
         if (s.ok() && e != cudaSuccess) s = cuda_status(e, "dist graph capture");
@@ -1243,7 +1247,7 @@ Status dist_run(decmg_gpu_dist* D, const Plan& plan, int nrhs, const double* h_b
         }
         cudaGraphExec_t ex = nullptr;
         DG_CUDA(cudaGraphInstantiate(&ex, gr, 0));
-        D->graphs.push_back({key, gr, ex, s1});
+        D->graphs.push_back({key, gr, ex, s1, kernels});
         ge = &D->graphs.back();
         return Status::Ok();
     };
@@ -1252,7 +1256,7 @@ Status dist_run(decmg_gpu_dist* D, const Plan& plan, int nrhs, const double* h_b
     auto step = [&]() -> Status {
         if (ge) {
             DG_CUDA(cudaGraphLaunch(ge->exec, st));
-            ++g->launch_count;
+            g->launch_count += ge->kernels;
             set_host_state(D, ge->post);
             return Status::Ok();
         }
