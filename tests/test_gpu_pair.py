@@ -43,7 +43,8 @@ PAIRED = [
 
 @pytest.mark.parametrize("base,nsub,dirichlet,nrhs", [("ico", 6, False, 16), ("ico", 7, False, 16),
                                                       ("ico", 8, False, 1), ("square", 9, True, 1),
-                                                      ("square", 8, True, 4)])
+                                                      ("square", 8, True, 4), ("ico", 7, False, 5),
+                                                      ("ico", 6, False, 32), ("equi:24:48:1.0", 4, False, 2)])
 @pytest.mark.parametrize("pre,post", [(2, 2), (3, 2), (2, 1), (4, 5)])
 def test_pair_iterates_bitwise(base, nsub, dirichlet, nrhs, pre, post):
     h0 = hierarchy({"DECMG_PAIR": "0"}, base, nsub, dirichlet=dirichlet, max_nrhs=nrhs)
