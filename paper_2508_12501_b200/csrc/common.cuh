@@ -208,7 +208,7 @@ struct decmg_gpu_ctx {
     // SMs with the persistent V-cycle kernels instead of holding them until they drain (DESIGN.md §5 x6)
     int carveout = 30;
     int vtail = 1;              // bottom of the V in one cooperative kernel (env DECMG_VTAIL=0: per-pass kernels)
-    int64_t vtail_items = 262144;  // ... from the first level with at most this many rows x RHS (env DECMG_VTAIL_ITEMS)
+    int64_t vtail_items = 32768;   // ... from the first level with at most this many thread items, rows x threads per row (env DECMG_VTAIL_ITEMS)
     int vtail_cta_items = 2048;    // ... levels with at most this many thread items on CTA 0 alone (env DECMG_VTAIL_CTA)
     int vtail_ctas_per_sm = 1;     // ... resident CTAs per SM, at most (env DECMG_VTAIL_CTAS)
     unsigned long long* vtail_trace = nullptr;  // per-pass %globaltimer stamps (env DECMG_VTAIL_TRACE=1)

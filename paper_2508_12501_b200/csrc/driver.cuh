@@ -584,7 +584,7 @@ struct Driver {
         if (!c->vtail || level < 1 || m < 1 || m >= kTailMax || tpr > 8 || fuse_hist) return false;
         if (c->lv.back().nv > 32) return false;  // larger coarse solves run the tree-sum grid CG
         if (plan.smoother != DECMG_SMOOTHER_JACOBI) return false;
-        if (static_cast<int64_t>(c->lv[level].nv) * nrhs > c->vtail_items) return false;
+        if (static_cast<int64_t>(c->lv[level].nv) * tpr > c->vtail_items) return false;  // (row, lane group) thread items
         if (w + 2 * m > static_cast<int>(plan.walk.size())) return false;
         for (int i = 0; i < m; ++i)
             if (plan.walk[w + i] != 'd' || plan.walk[w + m + i] != 'u') return false;
