@@ -232,3 +232,70 @@ def test_worked_example_hexagon_to_triangle():
     R[np.repeat(np.arange(3), np.diff(rrp)), rci] = rv
     np.testing.assert_array_equal(R, P.T / 2)
     np.testing.assert_allclose(h.apply(0, "R", np.ones(6)), 1.0, rtol=1e-13)
+
+
+# ---- solver known answers (proj/tests/test_multigrid.cpp) --------------------------------------
+# The coarse solve is the stand-in for Eigen's SparseLU; these are the reference's
+# contract tests at that boundary, which pin tolerances, not bits.
+
+def test_oracle_solver_contracts():
+    """zero data stays zero (151-164), two-level exactness with CG as an exact smoother (166-181), one-level
+    hierarchy = the direct solve (183-193), V-cycle contraction <= 0.5 for seeds 1-5 and bit-identical reruns
+    (195-227), exact preconditioner => PCG in <= 2 iterations (255-265), gmg_solve W(3,3) to 1e-10 (308-317),
+    pinned solve: residual <= 1e-12 and weighted mean <= 1e-10 (319-330)."""
+    o = OracleHierarchy("equi:4:8:1.0", 2)  # make_test_hierarchy(2): 289 / 81 / 25
+    n = o.n()
+    x, hist = o.run_cycles(np.zeros(n), np.zeros(n), ncycles=3, pre=3, post=3, smoother=1)
+    assert np.all(x == 0.0) and np.all(hist == 0.0)
+    for seed in range(1, 6):
+        b = o.project(o.rhs("lr", seed))
+        x, r = o.run_cycles(b, ncycles=10, pre=2, post=2, smoother=0)
+        for k in range(len(r) - 1):
+            if r[k] > 1e-10:
+                assert r[k + 1] <= 0.5 * r[k]
+        x2, r2 = o.run_cycles(b, ncycles=10, pre=2, post=2, smoother=0)
+        np.testing.assert_array_equal(r, r2)
+        np.testing.assert_array_equal(x, x2)
+    two = OracleHierarchy("equi:4:8:1.0", 1)  # fine 81, coarse 25
+    b = two.project(two.rhs("lr", 3))
+    _, r = two.run_cycles(b, ncycles=1, pre=4 * two.n(), post=4 * two.n(), smoother=3, walk="du")
+    assert r[-1] <= 1e-10
+    one = OracleHierarchy("equi:4:8:1.0", 0)
+    b = one.project(one.rhs("lr", 5))
+    _, r = one.run_cycles(b, ncycles=1, pre=3, post=3, smoother=1, walk="")
+    assert r[-1] <= 1e-12
+    _, hist, it, fin = one.pcg(one.rhs("lr", 7), 1e-9, 30, walk="", pre=3, post=3, smoother=1)
+    assert it <= 2 and fin <= 1e-9
+    b = o.project(o.rhs("lr", 23))
+    _, hist, it, fin = o.solve(b, tol=1e-10, max_cycles=50, pre=3, post=3, smoother=1)  # V here; W below on the GPU
+    assert it <= 50 and fin <= 1e-10
+    pin = OracleHierarchy("equi:2:4:1.0", 0)
+    b = pin.rhs("lr", 29)
+    xs = pin.coarse_solve(b)
+    area = pin.get(0, "dual_areas")
+    bp = pin.project(b)
+    res = bp - pin.spmv(0, "L", xs)
+    assert np.linalg.norm(res) <= 1e-12 * max(np.linalg.norm(bp), 1e-300)
+    assert abs(np.dot(area, xs)) <= 1e-10
+
+
+@pytest.mark.gpu
+def test_gpu_solver_contracts():
+    """The same contracts on the CUDA library (the cases test_gpu_parity.py::test_reference_unit_semantics does not
+    hold already): two-level exactness with CG smoothers, exact-preconditioner PCG, gmg_solve W(3,3) to 1e-10."""
+    import paper_2508_12501_b200 as d
+
+    two = d.MultigridHierarchy.from_base("equi:4:8:1.0", 1)
+    n = two.n()
+    plan = d.CyclePlan(walk=[d.Transition.Down, d.Transition.Up], pre=[4 * n] * 2, post=[4 * n] * 2,
+                       smoother=d.SmootherConfig(d.Smoother.Cg))
+    plan.cycles = 1
+    b = two.project_compatible(two.make_rhs("lr", 3))
+    assert two.run_cycle(plan, b, np.zeros(n)).residual_history[-1] <= 1e-10
+    one = d.MultigridHierarchy.from_base("equi:4:8:1.0", 0)
+    rep = d.gmg_preconditioned_cg(one, d.standard_plan(1, d.CycleKind.V), one.make_rhs("lr", 7), 1e-9, 30)
+    assert rep.converged and rep.iterations <= 2 and rep.final_relative_residual <= 1e-9
+    h = d.MultigridHierarchy.from_base("equi:4:8:1.0", 2)
+    rep = d.gmg_solve(h, d.standard_plan(h.levels(), d.CycleKind.W, 3, 3), h.project_compatible(h.make_rhs("lr", 23)),
+                      1e-10, 50)
+    assert rep.converged and rep.final_relative_residual <= 1e-10 and rep.iterations <= 50
