@@ -75,15 +75,17 @@ def test_pair_w_f_walks_bitwise(kindc):
     np.testing.assert_array_equal(got.x.view(np.uint64), ref.x.view(np.uint64))
 
 
+@pytest.mark.parametrize("pre,post", [(2, 2), (2, 1), (3, 3)])
 @pytest.mark.parametrize("base,nsub,dirichlet,nrhs", [("ico", 7, False, 16), ("square", 9, True, 1)])
-def test_pair_gmg_solve(base, nsub, dirichlet, nrhs):
+def test_pair_gmg_solve(base, nsub, dirichlet, nrhs, pre, post):
     """gmg_solve (solvers.cpp:251-279) with the fused norm inside the first pair: same cycle counts, bit-identical
-    solutions, histories to rounding; warm start and graph replays included (two solves per context)."""
+    solutions, histories to rounding; graph replays included (two solves per context). V(2,1) flips level 0's
+    ping-pong parity every cycle, so it runs the host-driven loop with its early exit after the pair."""
     h0 = hierarchy({"DECMG_PAIR": "0"}, base, nsub, dirichlet=dirichlet, max_nrhs=nrhs)
     h1 = hierarchy(PAIRED[0], base, nsub, dirichlet=dirichlet, max_nrhs=nrhs)
     kind = "sinsin" if dirichlet else "uniform"
     b = h0.make_rhs(kind, 11, nrhs) if nrhs > 1 else h0.make_rhs(kind, 11)
-    plan = d.standard_plan(h0.levels(), d.CycleKind.V, 2, 2, smoother=JAC)
+    plan = d.standard_plan(h0.levels(), d.CycleKind.V, pre, post, smoother=JAC)
     for _ in range(2):
         r0 = d.gmg_solve(h0, plan, b, 1e-8, 100)
         r1 = d.gmg_solve(h1, plan, b, 1e-8, 100)
