@@ -1,4 +1,4 @@
-"""One batched V(2,2) cycle at config 4 (16 RHS) bracketed by cudaProfilerStart/Stop,
+"""Three batched V(2,2) cycles at config 4 (16 RHS) bracketed by cudaProfilerStart/Stop,
 for an in-order ncu launch list:
   ncu --profile-from-start off --metrics gpu__time_duration.sum --csv python tools/cycle_launches.py"""
 import ctypes as C
@@ -18,7 +18,7 @@ plan = d.standard_plan(h.levels(), d.CycleKind.V, 2, 2, smoother=d.SmootherConfi
 plan.cycles = 2
 h.run_cycle(plan, B)
 cudart = C.CDLL("libcudart.so.12")
-plan.cycles = 1
+plan.cycles = 3  # the last one is a steady-state cycle (the first starts from x = 0)
 cudart.cudaProfilerStart()
 h.run_cycle(plan, B)
 cudart.cudaProfilerStop()

@@ -16,8 +16,8 @@ for r in rows:
 
 
 def short(n):
-    n = n.replace("decmg_gpu::", "").replace("<unnamed>::", "").replace("void ", "")
-    return re.sub(r"\(.*", "", n)
+    n = re.sub(r"\(.*", "", n.replace("void ", ""))
+    return re.sub(r"^.*?(?=k_|cub)", "", n)  # drop namespaces ("decmg_gpu::", "<unnamed>::" / "unnamed>::")
 
 
 seq = [(short(d["Kernel Name"]), d["Grid Size"], float(d["Metric Value"]) / 1000) for d in data]
