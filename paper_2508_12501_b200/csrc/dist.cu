@@ -1241,12 +1241,17 @@ Status dist_run(decmg_gpu_dist* D, const Plan& plan, int nrhs, const double* h_b
         const auto s1 = host_state(D);
         set_host_state(D, s0);  // nothing ran yet
         if (s.ok() && e != cudaSuccess) s = cuda_status(e, "dist graph capture");
-        if (!s.ok()) {
-            if (gr) cudaGraphDestroy(gr);
-            return s;
-        }
         cudaGraphExec_t ex = nullptr;
-        DG_CUDA(cudaGraphInstantiate(&ex, gr, 0));
+        if (s.ok() && cudaGraphInstantiate(&ex, gr, 0) != cudaSuccess) s = Status::Err(DECMG_CUDA, "dist graph instantiate");
+        if (!s.ok()) {
+            // a transport whose calls cannot be captured (nothing has run: the host state is restored):
+            // drop the graph for this context and run the cycles eagerly, as the first one did
+            if (gr) cudaGraphDestroy(gr);
+            cudaGetLastError();
+            g->graph = 0;
+            if (std::getenv("DECMG_DEBUG")) std::fprintf(stderr, "[decmg] dist: %s; cycles run eagerly\n", s.msg.c_str());
+            return Status::Ok();
+        }
         D->graphs.push_back({key, gr, ex, s1, kernels});
         ge = &D->graphs.back();
         return Status::Ok();
